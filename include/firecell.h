@@ -1,0 +1,197 @@
+/*
+ * firecell.h -- C ABI of the B200-native wildfire cellular-automaton path.
+ *
+ * Drop-in boundary for the reference's hot path (pyrocell 0.1.0; paths
+ * below are relative to /root/reference/pkg/src/pyrocell/).  The reference
+ * is pure Python/NumPy and has no FFI of its own: its "operator API" is the
+ * functions re-exported by __init__.py:4-98.  Each launcher here replaces the
+ * numerical core of one of those functions; the Python host layer
+ * (paper_2502_18738_b200/) binds them with ctypes and keeps the reference's
+ * signatures, argument meaning and exceptions.
+ *
+ * Rules: every pointer argument is DEVICE memory unless named host_*; the
+ * library never allocates (callers size buffers with the fc_*_bytes helpers);
+ * all launchers are asynchronous on the given stream and hold no global
+ * mutable state.  Return value: FC_OK, or FC_EINVAL (bad argument, nothing
+ * launched) / FC_ECUDA (launch error; fc_last_cuda_error() has the code).
+ *
+ * Data layout:
+ *   fire state    bit planes, tile-major: a 32x32-cell tile is 32 uint32 words
+ *                 (word r = row r, bit c = column c); planes are
+ *                 [M][tiles_y][tiles_x][32]. burning is double-buffered by
+ *                 step parity (burn[t & 1] holds pre-step-t state); burned is
+ *                 updated in place.  Padding cells outside HxW are "burned".
+ *   accumulator   fp32 [M][H][W]; t_ign int16 [M][H][W] (pre-step index of
+ *                 the step a cell ignited in; -1 initial/injected; 0x7FFF
+ *                 never); jacobian fp32 [M][H][W][4] = dp/d(c1,c2,a,p_h)
+ *                 captured at ignition on attached steps (0 elsewhere).
+ *   landscape     env fp32 [H][W][4] = {elevation m, wind speed m/s, wind
+ *                 direction deg East-CCW, vd=(1+canopy)(1+density)};
+ *                 env64 fp64 [H][W][5] = {elevation, speed, direction, canopy,
+ *                 density} read only by the fp64 guard recompute; optional
+ *                 slope tensors [H][W][8] (slot order NW,N,NE,W,E,SW,S,SE:
+ *                 slope in degrees from the source in that slot toward the
+ *                 target) replace the elevation-derived slope.
+ *   activity      flags int32 [M][TY][TX] = last pre-step index at which the
+ *                 tile must be visited; tile_list int32 [3][M*TY*TX] rotating
+ *                 compacted lists of tiles active at steps t, t+1, t+2 with
+ *                 list_count int32 [max_steps+3] (zeroed by fc_state_init).
+ *   params        fp64 [M][8] = {c1, c2, a, p_h, p_continue, norm_c, 0, 0}.
+ */
+#ifndef FIRECELL_H
+#define FIRECELL_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* fc_stream_t; /* == cudaStream_t */
+
+enum { FC_OK = 0, FC_EINVAL = 1, FC_ECUDA = 2 };
+
+/* Random draws (pyrocell/rng.py).  SPLITMIX reproduces rng.py:35-75 bit for
+ * bit (keyed by seed, step, absolute cell, channel); PHILOX is Philox4x32-10
+ * keyed by (seed, step, cell, member); INJECT consumes caller-supplied fp64
+ * draw tensors [nsteps][M][2][H][W] (channel 0 = ignite, 1 = continue). */
+enum { FC_RNG_SPLITMIX = 0, FC_RNG_PHILOX = 1, FC_RNG_INJECT = 2 };
+
+/* Slope source: on-the-fly from elevation (data_io.py:92-132 fused into the
+ * stencil) or the caller's per-slot slope tensor (model.py:88-90). */
+enum { FC_SLOPE_ELEVATION = 0, FC_SLOPE_TENSOR = 1 };
+
+#define FC_TILE 32
+#define FC_NPARAM 8
+#define FC_NCOUNTER 4 /* per member and step: ignitions, burn-outs, tiles, candidates */
+#define FC_T_NEVER 0x7FFF
+
+typedef struct {
+    int32_t height, width;    /* cells                                  */
+    int32_t tiles_y, tiles_x; /* ceil(height/32), ceil(width/32)         */
+    int32_t members;          /* independent simulations sharing the env */
+} fc_grid;
+
+typedef struct {
+    const float* env;       /* [H][W][4] fp32                           */
+    const double* env64;    /* [H][W][5] fp64                           */
+    const float* slope32;   /* [H][W][8] fp32, FC_SLOPE_TENSOR only     */
+    const double* slope64;  /* [H][W][8] fp64, FC_SLOPE_TENSOR only     */
+    double cell_side;       /* metres (kernel uses l and l*sqrt(2))     */
+    int32_t slope_mode;     /* FC_SLOPE_*                                */
+    int32_t slope_sign;     /* +1 downhill-positive, -1 uphill-positive */
+    int32_t factor_source;  /* vd at the source (1) or target (0) cell  */
+    int32_t pad_;
+} fc_landscape;
+
+typedef struct {
+    uint32_t* burn0;        /* [M][TY][TX][32] burning, even pre-steps  */
+    uint32_t* burn1;        /* [M][TY][TX][32] burning, odd pre-steps   */
+    uint32_t* burned;       /* [M][TY][TX][32]                          */
+    float* acc;             /* [M][H][W]                                */
+    int16_t* t_ign;         /* [M][H][W]                                */
+    float* jac;             /* [M][H][W][4], may be NULL (no gradients) */
+    int32_t* flags;         /* [M][TY][TX] last pre-step index active   */
+    int32_t* counters;      /* [M][max_steps][FC_NCOUNTER]              */
+    int32_t* tile_list;     /* [3][M*TY*TX] rotating active-tile lists  */
+    int32_t* list_count;    /* [max_steps+3] length of each step's list */
+    int32_t max_steps;
+    int32_t pad_;
+} fc_state;
+
+/* ------------------------------------------------------------ sizing --- */
+void fc_grid_make(int32_t height, int32_t width, int32_t members, fc_grid* out);
+size_t fc_plane_words(const fc_grid* g);              /* uint32 words per plane   */
+size_t fc_loss_workspace_bytes(const fc_grid* g, int32_t n_targets);
+
+/* -------------------------------------------------------------- state --- */
+/* new_fire_state (model.py:180-200) for every member: init is uint8 [M][H][W]
+ * (member_stride = H*W) or one [H][W] mask broadcast (member_stride = 0).
+ * t0 = pre-step index of the initial state.  Zeroes jac/counters. */
+int fc_state_init(const fc_grid* g, const fc_state* s, const uint8_t* init,
+                  int64_t member_stride, int32_t t0, fc_stream_t stream);
+
+/* Unpack state at pre-step index t to uint8 grids [M][H][W] (either may be
+ * NULL).  Mirrors FireState.burning / burned (model.py:158-160). */
+int fc_state_unpack(const fc_grid* g, const fc_state* s, int32_t t, uint8_t* burning,
+                    uint8_t* burned, fc_stream_t stream);
+
+/* inject_ignitions (kernel.py:405-419) before pre-step t: cells is int32
+ * [n][3] = (member, row, col), all in bounds (checked by the caller).
+ * Burnable cells start burning with accumulator 1.0 (a constant). */
+int fc_inject(const fc_grid* g, const fc_state* s, const int32_t* cells, int32_t n,
+              int32_t t, fc_stream_t stream);
+
+/* ------------------------------------------------------------ forward --- */
+/* Advance every member from pre-step index t0 by nsteps steps: the loop of
+ * run_simulation (kernel.py:504-524) over step_forward (kernel.py:263-333).
+ * host_attach: NULL or nsteps flags (step t0+i attaches when host_attach[i]).
+ * draws: FC_RNG_INJECT only, [nsteps][M][2][H][W] fp64.
+ * skip_inactive: 1 = only tiles near burning cells are visited (exact: the
+ * analogue of the reference's bounding-box window, kernel.py:296-302). */
+int fc_run(const fc_grid* g, const fc_landscape* land, const fc_state* s,
+           const double* params, const uint64_t* seeds, int32_t rng_mode,
+           const double* draws, int32_t t0, int32_t nsteps, const uint8_t* host_attach,
+           int32_t skip_inactive, fc_stream_t stream);
+
+/* ----------------------------------------------------------- backward --- */
+/* backward_params (tape.py:118-148): out[m][4] = sum_j g[m][j] * J[m][j] in
+ * (c1, c2, a, p_h) order; g is fp64 (g_is_f32 = 0) or fp32 [M][H][W].
+ * workspace: fc_loss_workspace_bytes(g, 1) bytes. */
+int fc_contract(const fc_grid* g, const fc_state* s, const void* dl_dacc, int32_t g_is_f32,
+                double* out, void* workspace, fc_stream_t stream);
+
+/* combined_loss (losses.py:44-86) summed over n_targets observation steps of
+ * one run, fused with the gradient contraction.  acc_s = acc where
+ * t_ign < obs_steps[k] (the accumulator as it stood after step obs_steps[k]);
+ * targets uint8 [n_targets][M][H][W] with member stride target_member_stride
+ * (0 = shared by all members).  Outputs per member m:
+ *   loss_out[m][2 + 2*n_targets] = {total, n_targets, bce_0, mse_0, bce_1, ...}
+ *   crop_out[m][n_targets][4] (int32 r0, r1, c0, c1; may be NULL)
+ *   grad_out[m][4]   (may be NULL: loss only)
+ *   dl_dacc [M][H][W] fp64 of the single target (n_targets == 1; may be NULL)
+ * workspace: fc_loss_workspace_bytes(g, n_targets) bytes. */
+int fc_loss_grad(const fc_grid* g, const fc_state* s, const uint8_t* targets,
+                 int64_t target_member_stride, const int32_t* host_obs_steps,
+                 int32_t n_targets, double* loss_out, int32_t* crop_out, double* grad_out,
+                 double* dl_dacc, void* workspace, fc_stream_t stream);
+
+/* combined_loss (losses.py:44-86) of a caller-supplied fp64 accumulator
+ * [H][W] and uint8 target: loss_out[4] = {total, 1, bce, mse}, crop_out[4],
+ * dl_dacc [H][W] fp64 (may be NULL).  workspace: fc_loss_workspace_bytes of
+ * a 1-member grid with 1 target. */
+int fc_loss_dense(int32_t height, int32_t width, const double* acc, const uint8_t* target,
+                  double* loss_out, int32_t* crop_out, double* dl_dacc, void* workspace,
+                  fc_stream_t stream);
+
+/* adamw_update + clamp_params (calibration.py:43-64, model.py:47-57) on the
+ * device params [M][8] with per-member moments adam[M][8] = {m[4], v[4]}.
+ * step = 1-based Adam step.  A non-finite gradient leaves that member's
+ * params untouched and sets status[m] = 1 (else 0). */
+int fc_adamw(const double* grads, double* params, double* adam, int32_t members,
+             int32_t step, double lr, double weight_decay, double beta1, double beta2,
+             double eps, int32_t clamp, int32_t* status, fc_stream_t stream);
+
+/* ---------------------------------------------------------------- rng --- */
+/* uniform_grid (rng.py:55-75) on the device: out [height][width] fp64. */
+int fc_uniform_grid(uint64_t seed, int64_t t, int32_t channel, int64_t row0, int64_t col0,
+                    int64_t height, int64_t width, double* out, fc_stream_t stream);
+/* derive_epoch_seed (rng.py:83-88); host function. */
+uint64_t fc_epoch_seed(uint64_t base_seed, uint64_t epoch);
+
+/* ------------------------------------------------------------- fields --- */
+/* build_fields (kernel.py:149-205) for the pyrocell API, evaluated in fp64
+ * with the reference's operation order for params row 0: out fp64 [8][H][W]
+ * (fp), or [5][8][H][W] (fp, raw, rest, cosm1, slope) with gradients. */
+int fc_build_fields(const fc_grid* g, const fc_landscape* land, const double* params,
+                    double* out, int32_t with_gradients, fc_stream_t stream);
+
+/* ---------------------------------------------------------- diagnostics --- */
+int fc_last_cuda_error(void);
+const char* fc_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FIRECELL_H */

@@ -1,0 +1,401 @@
+"""Device-resident landscape and fire state (the native B200 API).
+
+``DeviceLandscape`` holds the HBM layout of one landscape; ``FireBatch``
+holds M independent fire states sharing it (an ensemble; M = 1 for the
+reference's single-simulation API) and drives the kernels of
+libfirecell.so through the C ABI (include/firecell.h).  PyTorch provides
+device memory and streams only.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _lib as L
+
+# Slot order NW,N,NE,W,E,SW,S,SE (pyrocell/kernel.py:30-34)
+NEIGHBOR_POSITIONS = ((-1, -1), (-1, 0), (-1, 1), (0, -1), (0, 1), (1, -1), (1, 0), (1, 1))
+DEFAULT_NORM_C = 1.1486328125
+
+
+def _u64_to_i64(v: int) -> int:
+    v = int(v) & (2**64 - 1)
+    return v - 2**64 if v >= 2**63 else v
+
+
+def _dev(device) -> torch.device:
+    d = torch.device(device if device is not None else "cuda")
+    if d.type != "cuda":
+        raise RuntimeError("firecell runs on CUDA devices only (no CPU fallback)")
+    return d
+
+
+class DeviceLandscape:
+    """Environment rasters in the kernel's layout (see include/firecell.h).
+
+    env fp32 [H][W][4] = (elevation, wind speed, wind direction, vd) feeds the
+    fp32 fast path; env64 fp64 [H][W][5] = (elevation, speed, direction,
+    canopy, density) feeds the rare fp64 guard recompute; the optional slope
+    tensors [H][W][8] replace the elevation-derived slope.
+    """
+
+    def __init__(self, env: torch.Tensor, env64: torch.Tensor, *, cell_side: float = 30.0,
+                 slope32: Optional[torch.Tensor] = None, slope64: Optional[torch.Tensor] = None,
+                 slope_sign: int = 1, factor_site: str = "target"):
+        if factor_site not in ("target", "source"):
+            raise ValueError(f"factor_site must be 'target' or 'source', got {factor_site!r}")
+        self.env, self.env64 = env.contiguous(), env64.contiguous()
+        self.slope32 = None if slope32 is None else slope32.contiguous()
+        self.slope64 = None if slope64 is None else slope64.contiguous()
+        self.cell_side = float(cell_side)
+        self.slope_sign = -1 if slope_sign < 0 else 1
+        self.factor_site = factor_site
+        self.shape = tuple(env.shape[:2])
+
+    # ---------------------------------------------------------- builders
+    @classmethod
+    def from_elevation(cls, elevation, wind_speed, wind_direction, canopy, density, *,
+                       cell_side: float = 30.0, slope_sign: str = "downhill-positive",
+                       factor_site: str = "target", device=None) -> "DeviceLandscape":
+        """Elevation mode: slope derived on the fly per live pair (the fused
+        slope_from_altitude, pyrocell/data_io.py:92-132)."""
+        dev = _dev(device)
+        if slope_sign not in ("downhill-positive", "uphill-positive"):
+            raise ValueError(f"unknown slope_sign {slope_sign!r}")
+        if cell_side <= 0:
+            raise ValueError("cell_side must be > 0")
+        t64 = [torch.as_tensor(np.asarray(a) if not torch.is_tensor(a) else a).to(dev, torch.float64)
+               for a in (elevation, wind_speed, wind_direction, canopy, density)]
+        env64 = torch.stack(t64, dim=-1)
+        vd = (1.0 + t64[3]) * (1.0 + t64[4])
+        env = torch.stack([t64[0], t64[1], t64[2], vd], dim=-1).to(torch.float32)
+        return cls(env, env64, cell_side=cell_side,
+                   slope_sign=-1 if slope_sign == "uphill-positive" else 1,
+                   factor_site=factor_site)
+
+    @classmethod
+    def from_environment(cls, env, **kw) -> "DeviceLandscape":
+        return cls.from_elevation(env.elevation, env.wind_speed, env.wind_direction, env.canopy,
+                                  env.density, cell_side=env.cell_side, **kw)
+
+    @classmethod
+    def from_slope_tensor(cls, wind_speed, wind_direction, slope, canopy, density, *,
+                          cell_side: float = 30.0, factor_site: str = "target",
+                          slope_units: str = "degrees", device=None) -> "DeviceLandscape":
+        """Slope-tensor mode for the reference Landscape (model.py:76-105):
+        slope (H, W, 3, 3) degrees from each cell toward each neighbour."""
+        dev = _dev(device)
+        if slope_units not in ("degrees", "radians"):
+            raise ValueError(f"slope_units must be 'degrees' or 'radians', got {slope_units!r}")
+        sl = np.asarray(slope, dtype=np.float64)
+        if slope_units == "radians":
+            sl = np.degrees(sl)
+        h, w = sl.shape[:2]
+        # slot k at the source: slope toward the target = source - position
+        s8 = np.stack([sl[:, :, 1 - pr, 1 - pc] for pr, pc in NEIGHBOR_POSITIONS], axis=-1)
+        zeros = np.zeros((h, w))
+        base = cls.from_elevation(zeros, wind_speed, wind_direction, canopy, density,
+                                  cell_side=cell_side, factor_site=factor_site, device=dev)
+        s64 = torch.as_tensor(np.ascontiguousarray(s8)).to(dev)
+        base.slope64 = s64
+        base.slope32 = s64.to(torch.float32)
+        return base
+
+    def with_wind(self, wind_speed, wind_direction) -> "DeviceLandscape":
+        """Same landscape with replaced wind fields (WindUpdate, kernel.py:422-428)."""
+        dev = self.env.device
+        v = torch.as_tensor(np.asarray(wind_speed) if not torch.is_tensor(wind_speed) else wind_speed).to(dev, torch.float64)
+        d = torch.as_tensor(np.asarray(wind_direction) if not torch.is_tensor(wind_direction) else wind_direction).to(dev, torch.float64)
+        env64 = self.env64.clone()
+        env64[..., 1], env64[..., 2] = v, d
+        env = self.env.clone()
+        env[..., 1], env[..., 2] = v.to(torch.float32), d.to(torch.float32)
+        out = DeviceLandscape(env, env64, cell_side=self.cell_side, slope32=self.slope32,
+                              slope64=self.slope64, slope_sign=self.slope_sign,
+                              factor_site=self.factor_site)
+        return out
+
+    def struct(self) -> L.FcLandscape:
+        s = L.FcLandscape()
+        s.env, s.env64 = L.ptr(self.env), L.ptr(self.env64)
+        s.slope32, s.slope64 = L.ptr(self.slope32), L.ptr(self.slope64)
+        s.cell_side = self.cell_side
+        s.slope_mode = L.SLOPE_TENSOR if self.slope64 is not None else L.SLOPE_ELEVATION
+        s.slope_sign = self.slope_sign
+        s.factor_source = 1 if self.factor_site == "source" else 0
+        return s
+
+    @property
+    def nbytes(self) -> int:
+        return sum(t.numel() * t.element_size() for t in
+                   (self.env, self.env64, self.slope32, self.slope64) if t is not None)
+
+
+def pack_params(c1, c2, a, p_h, p_continue, norm_c=DEFAULT_NORM_C) -> list:
+    return [float(c1), float(c2), float(a), float(p_h), float(p_continue), float(norm_c), 0.0, 0.0]
+
+
+class FireBatch:
+    """M fire states on one landscape: bit planes, accumulator, ignition
+    steps, per-cell Jacobians, activity flags and per-step counters."""
+
+    def __init__(self, shape, members: int = 1, *, max_steps: int = 1024,
+                 with_jacobian: bool = False, device=None):
+        L.require_cuda()
+        dev = _dev(device)
+        self.device = dev
+        self.h, self.w = int(shape[0]), int(shape[1])
+        if self.h < 1 or self.w < 1:
+            raise ValueError(f"grid must be at least 1x1, got {shape}")
+        if max_steps >= L.T_NEVER:
+            raise ValueError(f"max_steps must be < {L.T_NEVER}")
+        self.m = int(members)
+        self.grid = L.grid(self.h, self.w, self.m)
+        words = L.lib().fc_plane_words(C.byref(self.grid))
+        self.planes = torch.empty((3, words), dtype=torch.int32, device=dev)
+        hw = self.h * self.w
+        self.acc = torch.zeros((self.m, self.h, self.w), dtype=torch.float32, device=dev)
+        self.t_ign = torch.empty((self.m, self.h, self.w), dtype=torch.int16, device=dev)
+        self.jac = (torch.zeros((self.m, self.h, self.w, 4), dtype=torch.float32, device=dev)
+                    if with_jacobian else None)
+        self.flags = torch.empty((self.m, self.grid.tiles_y, self.grid.tiles_x), dtype=torch.int32,
+                                 device=dev)
+        self.max_steps = int(max_steps)
+        self.counters = torch.zeros((self.m, self.max_steps, L.NCOUNTER), dtype=torch.int32,
+                                    device=dev)
+        ntiles = self.m * self.grid.tiles_y * self.grid.tiles_x
+        self.tile_list = torch.empty((3, ntiles), dtype=torch.int32, device=dev)
+        self.list_count = torch.zeros((self.max_steps + 3,), dtype=torch.int32, device=dev)
+        self.params = torch.zeros((self.m, L.NPARAM), dtype=torch.float64, device=dev)
+        self.seeds = torch.zeros((self.m,), dtype=torch.int64, device=dev)
+        self.adam = torch.zeros((self.m, 8), dtype=torch.float64, device=dev)
+        ws = max(L.lib().fc_loss_workspace_bytes(C.byref(self.grid), 8), 1 << 12)
+        self.workspace = torch.empty((ws,), dtype=torch.uint8, device=dev)
+        self.t = 0
+        self.init_burning = np.zeros(self.m, dtype=np.int64)
+        self._hw = hw
+
+    # ------------------------------------------------------------ plumbing
+    def struct(self) -> L.FcState:
+        s = L.FcState()
+        base, stride = self.planes.data_ptr(), self.planes.stride(0) * 4
+        s.burn0, s.burn1, s.burned = base, base + stride, base + 2 * stride
+        s.acc, s.t_ign, s.jac = L.ptr(self.acc), L.ptr(self.t_ign), L.ptr(self.jac)
+        s.flags, s.counters = L.ptr(self.flags), L.ptr(self.counters)
+        s.tile_list, s.list_count = L.ptr(self.tile_list), L.ptr(self.list_count)
+        s.max_steps = self.max_steps
+        return s
+
+    def set_params(self, params: Sequence, member: Optional[int] = None):
+        """params: 8-vectors (see pack_params) for every member or one."""
+        p = torch.as_tensor(np.asarray(params, dtype=np.float64), device=self.device)
+        if member is None:
+            self.params.copy_(p.reshape(-1, L.NPARAM).expand(self.m, L.NPARAM))
+        else:
+            self.params[member].copy_(p.reshape(L.NPARAM))
+
+    def set_seeds(self, seeds):
+        s = [_u64_to_i64(v) for v in np.atleast_1d(np.asarray(seeds, dtype=object))]
+        if len(s) == 1:
+            s = s * self.m
+        self.seeds.copy_(torch.tensor(s, dtype=torch.int64))
+
+    # -------------------------------------------------------------- state
+    def reset(self, init, t0: int = 0, stream=None):
+        """new_fire_state (model.py:180-200) for every member; init is a
+        (H, W) mask broadcast to all members or an (M, H, W) stack."""
+        if torch.is_tensor(init):
+            m8 = init.to(self.device, torch.uint8)
+        else:
+            m8 = torch.as_tensor(np.asarray(init, dtype=bool).astype(np.uint8), device=self.device)
+        if m8.dim() == 2:
+            if tuple(m8.shape) != (self.h, self.w):
+                raise ValueError(f"initial fire mask shape {tuple(m8.shape)} != landscape {(self.h, self.w)}")
+            stride = 0
+            per = int(m8.sum().item()) if not torch.cuda.is_current_stream_capturing() else 0
+            self.init_burning[:] = per
+        elif m8.dim() == 3 and tuple(m8.shape) == (self.m, self.h, self.w):
+            stride = self._hw
+            if not torch.cuda.is_current_stream_capturing():
+                self.init_burning[:] = m8.reshape(self.m, -1).sum(1).cpu().numpy()
+        else:
+            raise ValueError(f"initial fire mask must be 2-D or (M,H,W), got {tuple(m8.shape)}")
+        self._init_mask = m8.contiguous()
+        st = self.struct()
+        L.check(L.lib().fc_state_init(C.byref(self.grid), C.byref(st), L.ptr(self._init_mask),
+                                      stride, int(t0), L.stream_ptr(stream)), "fc_state_init")
+        self.t = int(t0)
+
+    def run(self, land: DeviceLandscape, nsteps: int, *, attach: Optional[Sequence[bool]] = None,
+            rng: str = "splitmix", draws: Optional[torch.Tensor] = None, skip_inactive: bool = True,
+            stream=None):
+        """Advance every member nsteps steps from the current pre-step index."""
+        if nsteps < 0:
+            raise ValueError("steps must be >= 0")
+        if land.shape != (self.h, self.w):
+            raise ValueError(f"state shape {(self.h, self.w)} != landscape {land.shape}")
+        if self.t + nsteps > self.max_steps:
+            raise ValueError(f"run past max_steps={self.max_steps}")
+        att = None
+        if attach is not None:
+            att_np = np.ascontiguousarray(np.asarray(attach, dtype=np.uint8)[:nsteps])
+            if att_np.any() and self.jac is None:
+                raise ValueError("attached steps need a FireBatch built with_jacobian=True")
+            att = att_np.ctypes.data_as(C.c_void_p)
+        mode = L.RNG_MODES[rng]
+        if mode == L.RNG_INJECT:
+            if draws is None or tuple(draws.shape) != (nsteps, self.m, 2, self.h, self.w):
+                raise ValueError("inject mode needs draws of shape (nsteps, M, 2, H, W)")
+            draws = draws.to(self.device, torch.float64).contiguous()
+        lst, st = land.struct(), self.struct()
+        L.check(L.lib().fc_run(C.byref(self.grid), C.byref(lst), C.byref(st), L.ptr(self.params),
+                               L.ptr(self.seeds), mode, L.ptr(draws), self.t, int(nsteps), att,
+                               1 if skip_inactive else 0, L.stream_ptr(stream)), "fc_run")
+        self.t += int(nsteps)
+        self._keep = (att_np if attach is not None else None, draws)  # lifetime until sync
+
+    def inject(self, cells, member: int = 0, stream=None):
+        """inject_ignitions (kernel.py:405-419) before the current step."""
+        rows = []
+        for cell in cells:
+            if len(cell) == 3:
+                m, r, c = (int(v) for v in cell)
+            else:
+                m, (r, c) = member, (int(cell[0]), int(cell[1]))
+            if not (0 <= r < self.h and 0 <= c < self.w):
+                raise IndexError(f"ignition cell ({r}, {c}) outside {self.h}x{self.w} grid")
+            rows.append((m, r, c))
+        if not rows:
+            return
+        t = torch.tensor(rows, dtype=torch.int32, device=self.device)
+        st = self.struct()
+        L.check(L.lib().fc_inject(C.byref(self.grid), C.byref(st), L.ptr(t), len(rows), self.t,
+                                  L.stream_ptr(stream)), "fc_inject")
+        self._inj = t
+
+    def unpack(self, stream=None):
+        """(burning, burned) uint8 tensors (M, H, W) at the current step."""
+        b = torch.empty((self.m, self.h, self.w), dtype=torch.uint8, device=self.device)
+        d = torch.empty_like(b)
+        st = self.struct()
+        L.check(L.lib().fc_state_unpack(C.byref(self.grid), C.byref(st), self.t, L.ptr(b),
+                                        L.ptr(d), L.stream_ptr(stream)), "fc_state_unpack")
+        return b, d
+
+    def series(self, t0: int = 0, t1: Optional[int] = None) -> np.ndarray:
+        """Per-step (burning, burned) counts after each step in [t0, t1)
+        (StepStats, kernel.py:431-439), from the device counters."""
+        t1 = self.t if t1 is None else t1
+        cnt = self.counters[:, :t1].to(torch.int64).cpu().numpy()
+        burning = self.init_burning[:, None] + np.cumsum(cnt[:, :, 0] - cnt[:, :, 1], axis=1)
+        burned = np.cumsum(cnt[:, :, 1], axis=1)
+        return np.stack([burning, burned], axis=-1)[:, t0:t1]
+
+    def attached_entries(self, attach_mask) -> int:
+        """Number of tape entries: ignitions on attached steps."""
+        cnt = self.counters[:, : self.t, 0].to(torch.int64).cpu().numpy()
+        mask = np.zeros(self.t, dtype=bool)
+        am = np.asarray(attach_mask, dtype=bool)
+        mask[: min(len(am), self.t)] = am[: self.t]
+        return int(cnt[:, mask].sum())
+
+    # ----------------------------------------------------------- backward
+    def contract(self, dl_dacc: torch.Tensor, stream=None) -> torch.Tensor:
+        """backward_params (tape.py:118-148): (M, 4) = sum_j dL/dacc_j J_j."""
+        if self.jac is None:
+            raise ValueError("no Jacobian recorded (FireBatch(with_jacobian=False))")
+        g = dl_dacc.to(self.device)
+        if g.dtype not in (torch.float32, torch.float64):
+            g = g.to(torch.float64)
+        g = g.reshape(self.m, self.h, self.w).contiguous()
+        out = torch.empty((self.m, 4), dtype=torch.float64, device=self.device)
+        st = self.struct()
+        L.check(L.lib().fc_contract(C.byref(self.grid), C.byref(st), L.ptr(g),
+                                    1 if g.dtype == torch.float32 else 0, L.ptr(out),
+                                    L.ptr(self.workspace), L.stream_ptr(stream)), "fc_contract")
+        self._keep_g = g
+        return out
+
+    def loss_grad(self, targets: torch.Tensor, obs_steps: Sequence[int], *, per_member=False,
+                  want_grad=True, want_dl_dacc=False, stream=None):
+        """combined_loss summed over observation steps, fused with the
+        gradient contraction.  targets: (S, H, W) shared or (S, M, H, W)."""
+        S = len(obs_steps)
+        tg = targets.to(self.device, torch.uint8).contiguous()
+        if tg.dim() == 2:
+            tg = tg[None]
+        if tg.shape[0] != S:
+            raise ValueError("one target per observation step")
+        if tg.dim() == 3:
+            if tuple(tg.shape[1:]) != (self.h, self.w):
+                raise ValueError(f"target shape {tuple(tg.shape[1:])} != accumulator {(self.h, self.w)}")
+            mstride = 0
+        else:
+            mstride = self._hw
+        obs = (C.c_int32 * S)(*[int(s) for s in obs_steps])
+        loss = torch.empty((self.m, 2 + 2 * S), dtype=torch.float64, device=self.device)
+        crop = torch.empty((self.m, S, 4), dtype=torch.int32, device=self.device)
+        grad = torch.empty((self.m, 4), dtype=torch.float64, device=self.device) if want_grad else None
+        dl = (torch.empty((self.m, self.h, self.w), dtype=torch.float64, device=self.device)
+              if want_dl_dacc else None)
+        st = self.struct()
+        L.check(L.lib().fc_loss_grad(C.byref(self.grid), C.byref(st), L.ptr(tg), mstride, obs, S,
+                                     L.ptr(loss), L.ptr(crop), L.ptr(grad), L.ptr(dl),
+                                     L.ptr(self.workspace), L.stream_ptr(stream)), "fc_loss_grad")
+        self._keep_t = tg
+        return loss, crop, grad, dl
+
+    def adamw(self, grads: torch.Tensor, step: int, lr: float, weight_decay: float = 0.0,
+              beta1=0.9, beta2=0.999, eps=1e-8, clamp=True, stream=None) -> torch.Tensor:
+        status = torch.zeros((self.m,), dtype=torch.int32, device=self.device)
+        L.check(L.lib().fc_adamw(L.ptr(grads), L.ptr(self.params), L.ptr(self.adam), self.m,
+                                 int(step), lr, weight_decay, beta1, beta2, eps, 1 if clamp else 0,
+                                 L.ptr(status), L.stream_ptr(stream)), "fc_adamw")
+        return status
+
+
+def loss_dense(acc: torch.Tensor, target: torch.Tensor, want_grad=True, stream=None):
+    """combined_loss (losses.py:44-86) of an arbitrary fp64 accumulator."""
+    L.require_cuda()
+    a = acc.to("cuda", torch.float64).contiguous()
+    y = target.to("cuda", torch.uint8).contiguous()
+    h, w = a.shape
+    g = L.grid(h, w, 1)
+    ws = torch.empty((max(L.lib().fc_loss_workspace_bytes(C.byref(g), 1), 4096),),
+                     dtype=torch.uint8, device=a.device)
+    loss = torch.empty((4,), dtype=torch.float64, device=a.device)
+    crop = torch.empty((4,), dtype=torch.int32, device=a.device)
+    dl = torch.empty_like(a) if want_grad else None
+    L.check(L.lib().fc_loss_dense(h, w, L.ptr(a), L.ptr(y), L.ptr(loss), L.ptr(crop), L.ptr(dl),
+                                  L.ptr(ws), L.stream_ptr(stream)), "fc_loss_dense")
+    return loss, crop, dl
+
+
+def uniform_grid_device(seed, t, channel, row0, col0, height, width, stream=None) -> torch.Tensor:
+    L.require_cuda()
+    if height < 0 or width < 0:
+        raise ValueError("negative window")
+    out = torch.empty((max(height, 0), max(width, 0)), dtype=torch.float64, device="cuda")
+    L.check(L.lib().fc_uniform_grid(int(seed) & (2**64 - 1), int(t), int(channel), int(row0),
+                                    int(col0), int(height), int(width), L.ptr(out),
+                                    L.stream_ptr(stream)), "fc_uniform_grid")
+    return out
+
+
+def build_fields_device(land: DeviceLandscape, params8, with_gradients=False, stream=None):
+    L.require_cuda()
+    h, w = land.shape
+    g = L.grid(h, w, 1)
+    p = torch.tensor(params8, dtype=torch.float64, device=land.env.device)
+    out = torch.empty(((5 if with_gradients else 1) * 8, h, w), dtype=torch.float64,
+                      device=land.env.device)
+    lst = land.struct()
+    L.check(L.lib().fc_build_fields(C.byref(g), C.byref(lst), L.ptr(p), L.ptr(out),
+                                    1 if with_gradients else 0, L.stream_ptr(stream)),
+            "fc_build_fields")
+    return out

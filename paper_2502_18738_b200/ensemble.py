@@ -1,0 +1,79 @@
+"""Ensemble forward runs from host buffers (the public call behind bench e2e).
+
+``EnsembleRunner`` keeps device buffers and pinned host staging between calls:
+each call uploads one landscape (fp32 rasters) and the initial mask, runs M
+members for `steps` steps on the device (libfirecell fc_run) and copies the
+final states, accumulators and per-step counts back to host memory.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+from .device import DEFAULT_NORM_C, DeviceLandscape, FireBatch, pack_params
+
+
+@dataclass
+class EnsembleResult:
+    burning: np.ndarray   # (M, H, W) uint8
+    burned: np.ndarray    # (M, H, W) uint8
+    accumulator: np.ndarray  # (M, H, W) fp32
+    series: np.ndarray    # (M, steps, 2) int64 (burning, burned after each step)
+
+
+def _pinned(shape, dtype):
+    return torch.empty(shape, dtype=dtype, pin_memory=True)
+
+
+class EnsembleRunner:
+    def __init__(self, shape, members: int, steps: int, *, cell_side: float = 30.0,
+                 rng: str = "splitmix", device=None):
+        self.h, self.w = shape
+        self.m, self.steps, self.rng = int(members), int(steps), rng
+        self.cell_side = cell_side
+        self.batch = FireBatch(shape, members, max_steps=max(steps, 1), device=device)
+        dev = self.batch.device
+        self.dev = dev
+        self.env_dev = torch.empty((5, self.h, self.w), dtype=torch.float32, device=dev)
+        self.init_dev = torch.empty((self.h, self.w), dtype=torch.uint8, device=dev)
+        self.out_b = _pinned((self.m, self.h, self.w), torch.uint8)
+        self.out_d = _pinned((self.m, self.h, self.w), torch.uint8)
+        self.out_acc = _pinned((self.m, self.h, self.w), torch.float32)
+        self.out_cnt = _pinned((self.m, max(steps, 1), 4), torch.int32)
+        self.h2d_bytes = self.env_dev.numel() * 4 + self.init_dev.numel()
+        self.d2h_bytes = (self.out_b.numel() * 2 + self.out_acc.numel() * 4
+                          + self.m * self.steps * 4 * 4)
+
+    def __call__(self, env_host: torch.Tensor, init_host: torch.Tensor, params: Sequence,
+                 seeds: Sequence[int], norm_c: float = DEFAULT_NORM_C,
+                 sync: bool = True) -> EnsembleResult:
+        """env_host: (5, H, W) fp32 (elevation, speed, direction, canopy,
+        density), ideally pinned; init_host: (H, W) uint8/bool;
+        params: per-member (c1, c2, a, p_h, p_continue)."""
+        self.env_dev.copy_(env_host, non_blocking=True)
+        self.init_dev.copy_(init_host, non_blocking=True)
+        e = self.env_dev
+        land = DeviceLandscape.from_elevation(e[0], e[1], e[2], e[3], e[4],
+                                              cell_side=self.cell_side, device=self.dev)
+        p8 = np.array([pack_params(*p, norm_c) for p in params], dtype=np.float64)
+        self.batch.set_params(p8.reshape(self.m, -1))
+        self.batch.set_seeds(list(seeds))
+        self.batch.reset(self.init_dev)
+        self.batch.run(land, self.steps, rng=self.rng)
+        b, d = self.batch.unpack()
+        self.out_b.copy_(b, non_blocking=True)
+        self.out_d.copy_(d, non_blocking=True)
+        self.out_acc.copy_(self.batch.acc, non_blocking=True)
+        self.out_cnt.copy_(self.batch.counters[:, : max(self.steps, 1)], non_blocking=True)
+        if sync:
+            torch.cuda.current_stream().synchronize()
+        cnt = self.out_cnt.numpy()[:, : self.steps].astype(np.int64)
+        init_n = int(np.asarray(init_host).sum()) if not torch.is_tensor(init_host) else \
+            int(init_host.sum())
+        burning = init_n + np.cumsum(cnt[:, :, 0] - cnt[:, :, 1], axis=1)
+        burned = np.cumsum(cnt[:, :, 1], axis=1)
+        return EnsembleResult(self.out_b.numpy(), self.out_d.numpy(), self.out_acc.numpy(),
+                              np.stack([burning, burned], axis=-1))

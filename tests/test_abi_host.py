@@ -1,0 +1,124 @@
+"""CPU tests: the C-ABI library loads and exports every symbol the header
+declares; host logic (attachment plans, params, AdamW, metrics, schedules)
+matches the reference goldens; device entry points refuse to run without a
+GPU (no CPU fallback)."""
+import math
+import re
+
+import numpy as np
+import pytest
+
+import paper_2502_18738_b200 as F
+from paper_2502_18738_b200 import _lib
+from golden_util import meta
+from oracle import oracle as O
+
+
+def test_header_and_library_exports():
+    hdr = open(_lib.HEADER).read()
+    declared = set(re.findall(r"\b(fc_[a-z_0-9]+)\s*\(", hdr))
+    assert declared == set(_lib.EXPORTS)
+    L = _lib.lib()
+    for name in _lib.EXPORTS:
+        assert hasattr(L, name), name
+    assert b"sm_100a" in L.fc_version()
+
+
+def test_library_is_sm100a_cubin():
+    import subprocess
+    out = subprocess.run(["cuobjdump", "--list-elf", _lib.SO_PATH], capture_output=True, text=True)
+    if out.returncode != 0:
+        pytest.skip("cuobjdump unavailable")
+    assert "sm_100a" in out.stdout
+
+
+def test_host_sizing_functions():
+    g = _lib.grid(2048, 2000, 16)
+    assert (g.tiles_y, g.tiles_x) == (64, 63)
+    import ctypes as C
+    assert _lib.lib().fc_plane_words(C.byref(g)) == 16 * 64 * 63 * 32
+    assert _lib.lib().fc_loss_workspace_bytes(C.byref(g), 4) > 0
+
+
+def test_epoch_seed_host_function_goldens():
+    # pyrocell tests/test_rng.py:16-23 and generated goldens
+    assert F.derive_epoch_seed(0, 0) == 5197578548964807871
+    assert F.derive_epoch_seed(2**63, 5) == 6872116035820236169
+    for b, e, want in meta()["epoch_seeds"]:
+        assert F.derive_epoch_seed(b, e) == want
+
+
+def test_attachment_plans_match_reference():
+    for total, rings, want in meta()["plans"]:
+        assert list(F.attachment_plan(total, F.StepRings(*rings))) == want
+    rings = F.StepRings(2, 3, 4)
+    plan = set(F.attachment_plan(20, rings))
+    for s in range(1, 21):
+        assert F.check_if_attach(s, 20, rings) == (s in plan)
+    with pytest.raises(ValueError):
+        F.check_if_attach(0, 10, F.StepRings())
+    with pytest.raises(ValueError):
+        F.StepRings(-1, 0, 0)
+
+
+def test_params_validation_and_clamp():
+    p = F.clamp_params(F.ModelParams(c1=2.0, c2=-1.0, a=0.5, p_h=0.1, p_continue=3.0))
+    assert (p.c1, p.c2, p.a, p.p_h, p.p_continue) == (1.0, 0.0, 0.5, 0.2, 3.0)
+    assert any("p_continue" in m for m in F.validate_params(p))
+    assert F.validate_params(F.ModelParams()) == []
+    st = F.new_fire_state(np.eye(3, dtype=bool))
+    assert st.t == 0 and st.accumulator[1, 1] == 1.0 and not st.burned.any()
+    with pytest.raises(ValueError):
+        F.new_fire_state(np.zeros(3, bool))
+
+
+def test_adamw_matches_oracle_restatement():
+    rng = np.random.default_rng(0)
+    st = F.AdamWState(learning_rate=0.01)
+    p = F.ModelParams()
+    ost, theta = {}, p.as_array()
+    for _ in range(5):
+        g = rng.standard_normal(4)
+        st, p = F.adamw_update(st, p, g)
+        theta = O.adamw_update(ost, theta, g, 0.01)
+        np.testing.assert_allclose(p.as_array(), theta, rtol=0, atol=0)
+    with pytest.raises(ValueError):
+        F.adamw_update(st, p, [np.nan, 0, 0, 0])
+
+
+def test_metrics_and_schedule():
+    a = np.zeros((4, 4), bool)
+    b = np.zeros((4, 4), bool)
+    a[0, :] = True
+    b[0, 2:] = True
+    b[1, :2] = True
+    assert F.jaccard_index(a, b) == 2 / 6
+    assert F.jaccard_index(np.zeros((2, 2), bool), np.zeros((2, 2), bool)) == 1.0
+    assert F.manhattan_distance([1, 2, 3], [1, 1, 1]) == 3
+    obs = [F.Observation(np.zeros((2, 2), bool), wind=(np.ones((2, 2)), np.zeros((2, 2)))),
+           F.Observation(np.zeros((2, 2), bool))]
+    sched = F.ObservationSchedule(obs, 5)
+    assert [u.apply_at_step for u in sched.wind_updates(2)] == [1]
+    with pytest.raises(ValueError):
+        F.ObservationSchedule(obs, 0)
+
+
+def test_scalar_semantics():
+    assert F.wind_factor(0.5, 0.7, 0.0, 33.0) == 1.0
+    assert F.wind_factor(0.045, 0.131, 8.0, 0.0) == math.exp(0.045 * 8.0)
+    assert math.isclose(F.wind_factor(0.045, 0.131, 8.0, 180.0), math.exp(0.36) * math.exp(-2.096),
+                        rel_tol=1e-12)
+    assert F.slope_factor(0.078, 0.0) == 1.0
+    assert F.ignition_prob([]) == 0.0 and F.ignition_prob([0.5, 0.5]) == 0.75
+    assert F.normalize_prob(0.5) == np.tanh(0.57431640625)
+    assert F.PROPAGATION_BEARINGS == (315.0, 270.0, 225.0, 0.0, 180.0, 45.0, 90.0, 135.0)
+
+
+def test_device_paths_refuse_cpu():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(RuntimeError):
+        F.FireBatch((8, 8))
+    with pytest.raises(RuntimeError):
+        F.uniform_grid(0, 0, 0, 0, 0, 2, 2)

@@ -1,0 +1,296 @@
+"""GPU parity: the sm_100a path (through libfirecell's C ABI) against the
+reference's frozen outputs (tests/golden/) and the CPU oracle.
+
+Bar (BASELINE.json north_star): fire-state grids bit-exact; burn
+probabilities and parameter gradients within 1e-5 relative (fp32 path).
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2502_18738_b200 as F
+from paper_2502_18738_b200 import synthetic as S
+from golden_util import P, RUN_CASES, case_kwargs, load, meta
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+RTOL_ACC = 1e-5    # fp32 accumulator vs fp64 reference (north_star)
+RTOL_GRAD = 1e-5   # parameter gradients (north_star)
+
+GOLDEN_DRAWS = {  # pyrocell tests/test_rng.py:7-14
+    (0, 0, 0, 0, 0): 0.23286544795475594,
+    (0, 0, 0, 0, 1): 0.991448890053859,
+    (1, 0, 0, 0, 0): 0.7828598730864468,
+    (0, 1, 0, 0, 0): 0.6289335415767472,
+    (0, 0, 5, 7, 0): 0.8443854602639748,
+    (12345, 99, 120, 250, 1): 0.5958213030105105,
+}
+
+
+def land_of(d, key_v="wind_speed", key_d="wind_direction"):
+    return F.Landscape(wind_speed=d[key_v], wind_direction=d[key_d], slope=d["slope"],
+                       canopy=d["canopy"], density=d["density"])
+
+
+def params_of(d):
+    c1, c2, a, ph, pc = (float(v) for v in d["params"])
+    return F.ModelParams(c1=c1, c2=c2, a=a, p_h=ph, p_continue=pc)
+
+
+def test_device_rng_goldens():
+    for (seed, t, r, c, ch), want in GOLDEN_DRAWS.items():
+        assert F.uniform_draw(seed, t, r, c, F.Channel(ch)) == want
+    m = meta()
+    assert F.uniform_grid(99, 4, F.Channel.IGNITE, 10, 20, 5, 6).tolist() == \
+        m["uniform_grid_99_4_I_10_20_5_6"]
+    assert F.uniform_grid(2**40 + 3, 123, 0, 70000, 3, 2, 3).tolist() == m["uniform_grid_bigseed"]
+    full = F.uniform_grid(5, 1, 1, 0, 0, 40, 40)
+    assert np.array_equal(F.uniform_grid(5, 1, 1, 13, 7, 9, 11), full[13:22, 7:18])
+
+
+@pytest.mark.parametrize("name", RUN_CASES)
+def test_run_simulation_matches_reference(name):
+    d = load(name)
+    kw = case_kwargs(name, d)
+    sched = [F.WindUpdate(a, v, w) for a, v, w in kw.pop("wind_schedule", [])]
+    tape = F.Tape(d["burning"].shape)
+    sim = F.run_simulation(land_of(d), params_of(d), d["init"], int(d["steps"]), int(d["seed"]),
+                           attach_steps=[int(s) for s in d["attach"]], tape=tape,
+                           wind_schedule=sched, **kw)
+    assert np.array_equal(sim.state.burning, d["burning"])
+    assert np.array_equal(sim.state.burned, d["burned"])
+    np.testing.assert_allclose(sim.state.accumulator, d["acc"], rtol=RTOL_ACC, atol=0)
+    assert np.array_equal(np.array([[s.burning, s.burned] for s in sim.series]).reshape(-1, 2),
+                          d["series"])
+    if "grad" in d:
+        assert tape.num_entries == int(d["num_entries"])
+        bd, g = F.combined_loss(sim.state.accumulator, d["target"])
+        assert math.isclose(bd.bce_term, float(d["bce"]), rel_tol=RTOL_ACC)
+        assert bd.crop_window == tuple(int(v) for v in d["crop"])
+        grad = F.backward_params(tape, g, F.DEFAULT_NORM_C)
+        for i in range(4):
+            if abs(d["grad"][i]) < 1e-12:
+                assert abs(grad[i]) < 1e-10
+            else:
+                assert abs(grad[i] - d["grad"][i]) <= RTOL_GRAD * abs(d["grad"][i]), (i, grad, d["grad"])
+
+
+def test_structural_zero_gradients():
+    d = load("run_windless")
+    tape = F.Tape(d["burning"].shape)
+    sim = F.run_simulation(land_of(d), params_of(d), d["init"], int(d["steps"]), int(d["seed"]),
+                           attach_steps=range(1, int(d["steps"]) + 1), tape=tape)
+    _, g = F.combined_loss(sim.state.accumulator, d["target"])
+    grad = F.backward_params(tape, g, F.DEFAULT_NORM_C)
+    assert grad[0] == 0.0 and grad[1] == 0.0 and grad[2] != 0.0
+
+
+def test_combined_loss_goldens():
+    bd, _ = F.combined_loss(np.zeros((8, 8)), np.zeros((8, 8), bool))
+    assert math.isclose(bd.bce_term, math.log(2.0), rel_tol=1e-12) and bd.mse_term == 0.0
+    assert bd.crop_window == (0, 8, 0, 8)
+    for name in ("loss_random", "loss_crop"):
+        d = load(name)
+        bd, g = F.combined_loss(d["acc"], d["target"])
+        assert math.isclose(bd.bce_term, float(d["bce"]), rel_tol=1e-12)
+        assert math.isclose(bd.mse_term, float(d["mse"]), rel_tol=1e-12, abs_tol=1e-300)
+        assert bd.crop_window == tuple(int(v) for v in d["crop"])
+        np.testing.assert_allclose(g, d["grad"], rtol=1e-12, atol=1e-16)
+
+
+def _bench_land(size, seed):
+    env = S.make_environment(size, seed=seed)
+    return env, F.DeviceLandscape.from_environment(env)
+
+
+@pytest.mark.parametrize("name", ["c0_small", "c0"])
+def test_config0_elevation_mode_matches_reference(name):
+    d = load(name)
+    size, steps = int(d["size"]), int(d["steps"])
+    env, dl = _bench_land(size, 0)
+    assert env.fingerprint() == str(d["fingerprint"])
+    b = F.FireBatch((size, size), 1, max_steps=steps)
+    b.set_params(F.pack_params(**{k: S.DEFAULT_BENCH_PARAMS[k] for k in
+                                  ("c1", "c2", "a", "p_h", "p_continue")}))
+    b.set_seeds([0])
+    b.reset(S.center_ignition(size))
+    b.run(dl, steps)
+    bu, bd = b.unpack()
+    assert np.array_equal(np.packbits(bu[0].bool().cpu().numpy()), d["burning"])
+    assert np.array_equal(np.packbits(bd[0].bool().cpu().numpy()), d["burned"])
+    acc = b.acc[0].double().cpu().numpy().ravel()
+    assert np.array_equal(np.flatnonzero(acc), d["acc_idx"])
+    np.testing.assert_allclose(acc[d["acc_idx"]], d["acc_val"], rtol=RTOL_ACC)
+    assert np.array_equal(b.series()[0], d["series"])
+
+
+def test_config2_iteration_fused_loss_grad():
+    d = load("c2_small")
+    size = int(d["size"])
+    env, dl = _bench_land(size, 2)
+    assert env.fingerprint() == str(d["fingerprint"])
+    b = F.FireBatch((size, size), 1, max_steps=100, with_jacobian=True)
+    b.set_params(F.pack_params(**{k: S.DEFAULT_BENCH_PARAMS[k] for k in
+                                  ("c1", "c2", "a", "p_h", "p_continue")}))
+    b.set_seeds([int(d["seed"])])
+    b.reset(S.center_ignition(size))
+    b.run(dl, 100, attach=[True] * 100)
+    bu, bd = b.unpack()
+    assert np.array_equal(bu[0].bool().cpu().numpy(), d["burning"])
+    assert np.array_equal(bd[0].bool().cpu().numpy(), d["burned"])
+    loss, crop, grad, _ = b.loss_grad(torch.as_tensor(d["targets"]), [int(s) for s in d["obs"]])
+    assert math.isclose(float(loss[0, 0]), float(d["loss"]), rel_tol=RTOL_ACC)
+    np.testing.assert_allclose(grad[0].cpu().numpy(), d["grad"], rtol=RTOL_GRAD)
+
+
+def test_calibrate_trajectory_matches_reference():
+    d = load("calibrate_small")
+    size = int(d["size"])
+    env = S.make_environment(size, seed=5)
+    arr = S.reference_landscape_arrays(env, O.slope_from_altitude)
+    land = F.Landscape(**arr)
+    sched = F.ObservationSchedule([F.Observation(target=t) for t in d["targets"]], 6)
+    start = F.ModelParams(c1=0.0, c2=0.0, a=0.0, p_h=0.3, p_continue=0.5)
+    res = F.calibrate(land, S.center_ignition(size), sched, start, F.StepRings(1, 2, 3),
+                      max_epochs=3, base_seed=5, learning_rate=0.05)
+    assert res.manifest.epoch_seeds == [int(s) for s in d["epoch_seeds"]]
+    rec = np.array([[r.epoch, r.iteration, r.loss, r.bce, r.mse, r.jaccard, r.manhattan]
+                    for r in res.records])
+    np.testing.assert_array_equal(rec[:, [0, 1, 5, 6]], d["records"][:, [0, 1, 5, 6]])
+    np.testing.assert_allclose(rec[:, 2:5], d["records"][:, 2:5], rtol=1e-5)
+    traj = np.array([[e, i, p.c1, p.c2, p.a, p.p_h, p.p_continue]
+                     for e, i, p in res.manifest.trajectory])
+    np.testing.assert_allclose(traj, d["trajectory"], rtol=1e-4, atol=1e-6)
+
+
+def _oracle_vs_device(size_h, size_w, steps, seed, attach, members=1, env_seed=9, skip=True,
+                      rng="splitmix", draws=None, params=None):
+    env = S.make_environment(size_h, size_w, seed=env_seed)
+    dl = F.DeviceLandscape.from_environment(env)
+    arr = S.reference_landscape_arrays(env, O.slope_from_altitude)
+    p = params or P([0.045, 0.131, 0.078, 0.58, 0.3])
+    init = S.center_ignition(size_h, size_w)
+    b = F.FireBatch((size_h, size_w), members, max_steps=steps, with_jacobian=attach)
+    b.set_params(F.pack_params(p.c1, p.c2, p.a, p.p_h, p.p_continue))
+    b.set_seeds([seed + m for m in range(members)])
+    b.reset(init)
+    b.run(dl, steps, attach=[attach] * steps, skip_inactive=skip, rng=rng, draws=draws)
+    return env, arr, p, init, b
+
+
+def test_ragged_grid_members_and_partition_invariance():
+    h, w, steps = 201, 333, 120
+    _, arr, p, init, b = _oracle_vs_device(h, w, steps, 40, True, members=3)
+    bu, bd = (x.bool().cpu().numpy() for x in b.unpack())
+    for m in range(3):
+        res = O.run(**arr, params=p, init=init, steps=steps, seed=40 + m,
+                    attach_steps=range(1, steps + 1), threads=4)
+        assert np.array_equal(bu[m], res.burning) and np.array_equal(bd[m], res.burned)
+        np.testing.assert_allclose(b.acc[m].double().cpu().numpy(), res.acc, rtol=RTOL_ACC)
+        assert np.array_equal(b.series()[m], res.series)
+        jac = b.jac[m].double().cpu().numpy()
+        g = np.random.default_rng(m).standard_normal((h, w))
+        got = b.contract(torch.as_tensor(np.stack([g * (k == m) for k in range(3)])))[m]
+        want = O.contract(res.jac, g)
+        np.testing.assert_allclose(got.cpu().numpy(), want, rtol=RTOL_GRAD)
+        np.testing.assert_allclose(jac, res.jac, rtol=2e-4, atol=1e-6)
+    # dense sweep (no activity skipping) must give identical bytes
+    _, _, _, _, b2 = _oracle_vs_device(h, w, steps, 40, True, members=3, skip=False)
+    assert torch.equal(b.planes, b2.planes)
+    assert torch.equal(b.acc, b2.acc) and torch.equal(b.t_ign, b2.t_ign)
+    assert torch.equal(b.jac, b2.jac)
+
+
+def test_draw_injection_mode_bit_exact():
+    h, w, steps = 64, 80, 40
+    env = S.make_environment(h, w, seed=4)
+    draws = np.stack([np.stack([O.uniform_grid(11, t, ch, 0, 0, h, w) for ch in (0, 1)])
+                      for t in range(steps)])[:, None]
+    _, _, _, _, a = _oracle_vs_device(h, w, steps, 11, False, env_seed=4)
+    _, _, _, _, b = _oracle_vs_device(h, w, steps, 11, False, env_seed=4, rng="inject",
+                                      draws=torch.as_tensor(draws))
+    assert torch.equal(a.planes, b.planes) and torch.equal(a.acc, b.acc)
+
+
+@pytest.mark.parametrize("rng", ["splitmix", "philox"])
+def test_ignition_frequency(rng):
+    # one burning cell, one burnable neighbour, 4000 members (independent
+    # draws): frequency realises p within 4 sigma (tests/test_kernel.py:286-303)
+    n = 4000
+    zeros = np.zeros((1, 2))
+    dl = F.DeviceLandscape.from_elevation(zeros, zeros, zeros, zeros, zeros)
+    b = F.FireBatch((1, 2), n, max_steps=1)
+    b.set_params(F.pack_params(0.045, 0.131, 0.078, 0.4, 1.0))
+    b.set_seeds(list(range(n)))
+    init = np.zeros((1, 2), bool)
+    init[0, 0] = True
+    b.reset(init)
+    b.run(dl, 1, rng=rng)
+    hits = int(b.unpack()[0][:, 0, 1].sum())
+    p = float(np.tanh(F.DEFAULT_NORM_C * 0.4))
+    assert abs(hits / n - p) < 4 * math.sqrt(p * (1 - p) / n)
+
+
+def test_fire_model_algorithm1_gradients():
+    from paper_2502_18738_b200.torch_model import FireModel, combined_loss_torch
+    d = load("run_rand16")
+    land = land_of(d)
+    dl = F.DeviceLandscape.from_slope_tensor(land.wind_speed, land.wind_direction, land.slope,
+                                             land.canopy, land.density)
+    pr = params_of(d)
+    model = FireModel(dl, d["init"], a=pr.a, c1=pr.c1, c2=pr.c2, p_h=pr.p_h,
+                      p_continue=pr.p_continue, seed=int(d["seed"]))
+    for _ in range(int(d["steps"])):
+        model.compute(attach=True)
+    loss = combined_loss_torch(model.accumulator, torch.as_tensor(d["target"]))
+    loss.backward()
+    got = np.array([model.c_1.grad.item(), model.c_2.grad.item(), model.a.grad.item(),
+                    model.p_h.grad.item()])
+    np.testing.assert_allclose(got, d["grad"], rtol=RTOL_GRAD)
+    assert model.p_continue.grad.item() == 0.0
+    assert math.isclose(loss.item(), float(d["bce"]) + float(d["mse"]), rel_tol=RTOL_ACC)
+    opt = torch.optim.AdamW(model.parameters(), lr=5e-3)
+    opt.step()
+    opt.zero_grad()
+    model.clamp_()
+    model.reset(seed=model.seed)
+    assert model.t == 0
+
+
+def test_inject_and_step_forward_api():
+    d = load("run_rand9_source")
+    land = land_of(d)
+    params = params_of(d)
+    st = F.new_fire_state(np.zeros(land.shape, bool), land)
+    F.inject_ignitions(st, [(4, 4)])
+    for _ in range(int(d["steps"])):
+        F.step_forward(st, land, params, int(d["seed"]), factor_site="source")
+    assert np.array_equal(st.burning, d["burning"]) and np.array_equal(st.burned, d["burned"])
+    np.testing.assert_allclose(st.accumulator, d["acc"], rtol=RTOL_ACC)
+    with pytest.raises(IndexError):
+        F.inject_ignitions(st, [(9, 0)])
+    b = F.FireBatch(land.shape, 1, max_steps=4)
+    b.reset(np.zeros(land.shape, bool))
+    with pytest.raises(IndexError):
+        b.inject([(0, 9)])
+    b.inject([(2, 2)])
+    assert int(b.unpack()[0].sum()) == 1 and float(b.acc[0, 2, 2]) == 1.0
+
+
+def test_build_fields_matches_oracle_formula():
+    d = load("run_rand16")
+    land = land_of(d)
+    pr = params_of(d)
+    f = F.build_fields(land, pr, with_gradients=True)
+    # field k at source i toward target i - pos[k], against the scalar formula
+    for (r, c) in [(3, 4), (8, 8), (0, 5), (15, 15)]:
+        for k, (pr_, pc_) in enumerate(F.NEIGHBOR_POSITIONS):
+            tr, tc = r - pr_, c - pc_
+            if not (0 <= tr < 16 and 0 <= tc < 16):
+                continue
+            raw = F.propagate_prob(pr, land, (r, c), (tr, tc))
+            assert math.isclose(f.raw[k][r, c], raw, rel_tol=1e-12)
+            assert math.isclose(f.fp[k][r, c], float(F.normalize_prob(raw)), rel_tol=1e-12)
