@@ -31,6 +31,7 @@ sys.path.insert(0, REPO)
 
 H = W = 2048
 MEMBERS = 16
+WINDOW = 8  # CA steps fused per kernel launch (temporal blocking)
 STEPS = 500
 CELL_UPDATES_PER_MEMBER = H * W * STEPS
 METRIC = "cell-updates/sec (fwd) & fwd+bwd calibration iter/s at 1/2/4/8 B200; % of HBM BW"
@@ -39,7 +40,7 @@ CONFIG = {"workload": "c1_ensemble_forward", "members_per_gpu": MEMBERS, "grid":
           "params": "a=0.078 c1=0.045 c2=0.131 p_h=0.58*U[0.9,1.1] p_continue=0.3",
           "env": "synthetic config-0 generator at 2048^2 (seeded)",
           "l2": "flushed (256 MiB write) before every timed step",
-          "activity_skipping": True}
+          "activity_skipping": True, "steps_per_launch": WINDOW}
 
 
 def parse():
@@ -187,31 +188,41 @@ def timed_loop(fn, K, flush):
     return [a.elapsed_time(b) for a, b in times]
 
 
-def per_launch_profile(batch, land, steps):
-    """Average step-kernel duration with CUDA events around each launch on
-    the launching stream (one launch per fc_run call), plus the counters."""
+def launch_bytes(cnt, burning_pre, window, tiles_override=None):
+    """Algorithmic bytes of each window launch from the per-step counters:
+    512 B per visited 32x32 tile (burning + burned words read and written
+    once per launch), 16 B of env per ignition candidate and per burning
+    source cell per step, 6 B (acc + t_ign) per ignition."""
+    steps = cnt.shape[0]
+    out = []
+    for a in range(0, steps, window):
+        b = min(a + window, steps)
+        tiles = cnt[a, 2] if tiles_override is None else tiles_override
+        out.append(512.0 * tiles + 16.0 * (cnt[a:b, 3].sum() + burning_pre[a:b].sum())
+                   + 6.0 * cnt[a:b, 0].sum())
+    return np.array(out)
+
+
+def per_launch_profile(batch, land, steps, window, skip=True):
+    """Average window-kernel duration with CUDA events around each launch
+    on the launching stream (one launch per fc_run call of `window` steps)."""
     import torch
     st = torch.cuda.current_stream()
     batch.reset(batch._init_mask)
     evs = []
-    for _ in range(steps):
+    for a in range(0, steps, window):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(st)
-        batch.run(land, 1)
+        batch.run(land, min(window, steps - a), window=window, skip_inactive=skip)
         e1.record(st)
         evs.append((e0, e1))
     torch.cuda.synchronize()
     ms = np.array([a.elapsed_time(b) for a, b in evs])
     cnt = batch.counters[:, :steps].to(torch.int64).sum(0).cpu().numpy()  # (steps, 4)
     ser = batch.series()  # (M, steps, 2)
-    burning_pre = np.concatenate([[batch.init_burning.sum()],
-                                  ser[:, :-1, 0].sum(0)])[:steps]
-    # algorithmic bytes per launch: 4 bit-plane words per visited tile row
-    # (burning read + write, burned read + write) = 512 B per 32x32 tile;
-    # 16 B of env per candidate and per burning source cell; 6 B (acc +
-    # t_ign) per ignition.
-    bytes_ = 512.0 * cnt[:, 2] + 16.0 * (cnt[:, 3] + burning_pre) + 6.0 * cnt[:, 0]
-    return ms, bytes_, cnt
+    burning_pre = np.concatenate([[batch.init_burning.sum()], ser[:, :-1, 0].sum(0)])[:steps]
+    tiles = None if skip else batch.m * batch.grid.tiles_y * batch.grid.tiles_x
+    return ms, launch_bytes(cnt, burning_pre, window, tiles), cnt
 
 
 def run_ours(args):
@@ -242,7 +253,7 @@ def run_ours(args):
 
     def one_run():
         batch.reset(init_dev)
-        batch.run(dl, STEPS)
+        batch.run(dl, STEPS, window=WINDOW)
 
     for _ in range(args.warmup):
         one_run()
@@ -256,21 +267,21 @@ def run_ours(args):
     total_ms = allreduce_max(float(sum(ms)), dev)
     cu = world * MEMBERS * CELL_UPDATES_PER_MEMBER * args.steps
     value = cu / (total_ms / 1e3)
-    launches_per_step = 3 + STEPS  # pack/init/flags kernels + one step kernel per CA step
+    launches_per_step = 3 + (STEPS + WINDOW - 1) // WINDOW  # reset kernels + window launches
 
     # final-state sanity (affected counts) for the log
     ser = batch.series()
     affected_final = int(ser[:, -1].sum())
 
     # -------------------------------------------------- roofline (live)
-    lms, lbytes, cnt = per_launch_profile(batch, dl, STEPS)
+    lms, lbytes, cnt = per_launch_profile(batch, dl, STEPS, WINDOW)
     achieved = float(lbytes.sum() / (lms.sum() / 1e3)) / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
-                "kernel": "step_kernel<SPLITMIX,elev,no-attach>",
+                "kernel": f"window_kernel<SPLITMIX,elev,no-attach,K={WINDOW}>",
                 "avg_launch_us": float(1e3 * lms.mean()),
                 "algorithmic_bytes_per_launch": float(lbytes.mean()),
-                "tiles_visited_per_launch": float(cnt[:, 2].mean()),
+                "tiles_visited_per_launch": float(cnt[::WINDOW, 2].mean()),
                 "note": "activity-skipping sweep: only tiles near fire are visited, so the "
                         "launch is latency-bound; see dense_probe for the full-domain sweep"}
     prof = os.path.join(REPO, "profiles", "ncu_traffic.json")
@@ -386,8 +397,9 @@ def bench_calibration(dev):
 
 def bench_dense(dev, peak):
     """Config 3 on one GPU: 16384^2, 8 random 5x5 ignitions, sigma x32 env
-    (FFT on the device); per-launch time of the dense sweep (every tile, the
-    HBM-bound regime) and of the activity-skipping sweep."""
+    (FFT on the device).  Window kernel (K=8) timed per launch with CUDA
+    events, once visiting every tile (the HBM-streaming regime) and once
+    with activity lists."""
     import torch
 
     import paper_2502_18738_b200 as F
@@ -398,39 +410,28 @@ def bench_dense(dev, peak):
                                           e["canopy"], e["density"], device=dev)
     del e
     init = torch.as_tensor(S.random_blocks(n, n, 8, 5, seed=3).astype(np.uint8), device=dev)
-    out = {"grid": [n, n], "steps": steps}
+    out = {"grid": [n, n], "steps": steps, "steps_per_launch": WINDOW}
     for skip in (False, True):
         b = F.FireBatch((n, n), 1, max_steps=steps, device=dev)
         b.set_params(F.pack_params(0.045, 0.131, 0.078, 0.58, 0.3))
         b.set_seeds([3])
         b.reset(init)
-        b.run(dl, 5, skip_inactive=skip)  # warm-up
+        b.run(dl, 2 * WINDOW, window=WINDOW, skip_inactive=skip)  # warm-up
         b.reset(init)
+        b._init_mask = init
         torch.cuda.synchronize()
-        st = torch.cuda.current_stream()
-        evs = []
-        for _ in range(steps):
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(st)
-            b.run(dl, 1, skip_inactive=skip)
-            e1.record(st)
-            evs.append((e0, e1))
-        torch.cuda.synchronize()
-        ms = np.array([a.elapsed_time(c) for a, c in evs])
-        cnt = b.counters[0, :steps].to(torch.int64).cpu().numpy()
-        cells = n * n
-        key = "skip" if skip else "dense"
-        byts = 512.0 * cnt[:, 2] + 16.0 * cnt[:, 3] + 6.0 * cnt[:, 0]
+        ms, byts, cnt = per_launch_profile(b, dl, steps, WINDOW, skip)
         ach = float(byts.sum() / (ms.sum() / 1e3)) / 1e9
+        key = "skip" if skip else "dense"
         out[key] = {"avg_launch_us": float(1e3 * ms.mean()),
-                    "cell_updates_per_s": cells * steps / (ms.sum() / 1e3),
+                    "cell_updates_per_s": n * n * steps / (ms.sum() / 1e3),
                     "achieved_GBps": ach, "frac_of_peak": ach / peak,
                     "bytes_per_launch": float(byts.mean()),
-                    "tiles_per_launch": float(cnt[:, 2].mean())}
+                    "tiles_per_launch": float(n * n / 1024 if not skip else cnt[::WINDOW, 2].mean())}
         del b
-    out["note"] = ("dense = every 32x32 tile visited each step (0.5 B/cell-update of bit-plane "
-                   "traffic); the SURVEY's 18 B/cell-update fp32-field layout would cap the same "
-                   "sweep at peak/18")
+    out["note"] = ("dense = every 32x32 tile visited each launch (512 B per tile per launch of "
+                   "bit-plane traffic = 0.5/K B per cell-update); the SURVEY's 18 B/cell-update "
+                   "fp32-field design would cap the same sweep at peak/18 = 3.6e11 cu/s")
     return out
 
 

@@ -25,8 +25,9 @@
  *                 the step a cell ignited in; -1 initial/injected; 0x7FFF
  *                 never); jacobian fp32 [M][H][W][4] = dp/d(c1,c2,a,p_h)
  *                 captured at ignition on attached steps (0 elsewhere).
- *   landscape     env fp32 [H][W][4] = {elevation m, wind speed m/s, wind
- *                 direction deg East-CCW, vd=(1+canopy)(1+density)};
+ *   landscape     env fp32 [H][W][4] = {elevation m, wind vector east and
+ *                 north m/s (speed * cos/sin of the direction, deg East-CCW),
+ *                 vd=(1+canopy)(1+density)};
  *                 env64 fp64 [H][W][5] = {elevation, speed, direction, canopy,
  *                 density} read only by the fp64 guard recompute; optional
  *                 slope tensors [H][W][8] (slot order NW,N,NE,W,E,SW,S,SE:
@@ -74,7 +75,7 @@ typedef struct {
 } fc_grid;
 
 typedef struct {
-    const float* env;       /* [H][W][4] fp32                           */
+    const float* env;       /* [H][W][4] fp32 {E, wind east, north, vd}  */
     const double* env64;    /* [H][W][5] fp64                           */
     const float* slope32;   /* [H][W][8] fp32, FC_SLOPE_TENSOR only     */
     const double* slope64;  /* [H][W][8] fp64, FC_SLOPE_TENSOR only     */
@@ -112,16 +113,18 @@ size_t fc_loss_workspace_bytes(const fc_grid* g, int32_t n_targets);
 int fc_state_init(const fc_grid* g, const fc_state* s, const uint8_t* init,
                   int64_t member_stride, int32_t t0, fc_stream_t stream);
 
-/* Unpack state at pre-step index t to uint8 grids [M][H][W] (either may be
- * NULL).  Mirrors FireState.burning / burned (model.py:158-160). */
-int fc_state_unpack(const fc_grid* g, const fc_state* s, int32_t t, uint8_t* burning,
+/* Unpack the current state to uint8 grids [M][H][W] (either may be NULL);
+ * phase = number of fc_run launches since fc_state_init (selects the
+ * burning buffer).  Mirrors FireState.burning / burned (model.py:158-160). */
+int fc_state_unpack(const fc_grid* g, const fc_state* s, int32_t phase, uint8_t* burning,
                     uint8_t* burned, fc_stream_t stream);
 
-/* inject_ignitions (kernel.py:405-419) before pre-step t: cells is int32
- * [n][3] = (member, row, col), all in bounds (checked by the caller).
- * Burnable cells start burning with accumulator 1.0 (a constant). */
+/* inject_ignitions (kernel.py:405-419) before pre-step t (launch phase
+ * `phase`): cells is int32 [n][3] = (member, row, col), all in bounds
+ * (checked by the caller).  Burnable cells start burning with accumulator
+ * 1.0 (a constant). */
 int fc_inject(const fc_grid* g, const fc_state* s, const int32_t* cells, int32_t n,
-              int32_t t, fc_stream_t stream);
+              int32_t t, int32_t phase, fc_stream_t stream);
 
 /* ------------------------------------------------------------ forward --- */
 /* Advance every member from pre-step index t0 by nsteps steps: the loop of
@@ -129,11 +132,13 @@ int fc_inject(const fc_grid* g, const fc_state* s, const int32_t* cells, int32_t
  * host_attach: NULL or nsteps flags (step t0+i attaches when host_attach[i]).
  * draws: FC_RNG_INJECT only, [nsteps][M][2][H][W] fp64.
  * skip_inactive: 1 = only tiles near burning cells are visited (exact: the
- * analogue of the reference's bounding-box window, kernel.py:296-302). */
+ * analogue of the reference's bounding-box window, kernel.py:296-302).
+ * window: steps fused per launch (temporal blocking; 1, 4, 8 or 16).
+ * host_phase: in/out launch counter (see fc_state_unpack). */
 int fc_run(const fc_grid* g, const fc_landscape* land, const fc_state* s,
            const double* params, const uint64_t* seeds, int32_t rng_mode,
            const double* draws, int32_t t0, int32_t nsteps, const uint8_t* host_attach,
-           int32_t skip_inactive, fc_stream_t stream);
+           int32_t skip_inactive, int32_t window, int32_t* host_phase, fc_stream_t stream);
 
 /* ----------------------------------------------------------- backward --- */
 /* backward_params (tape.py:118-148): out[m][4] = sum_j g[m][j] * J[m][j] in

@@ -90,8 +90,8 @@ def lib():
             "fc_loss_workspace_bytes": (C.c_size_t, [G, i32]),
             "fc_state_init": (C.c_int, [G, ST, vp, i64, i32, vp]),
             "fc_state_unpack": (C.c_int, [G, ST, i32, vp, vp, vp]),
-            "fc_inject": (C.c_int, [G, ST, vp, i32, i32, vp]),
-            "fc_run": (C.c_int, [G, LS, ST, vp, vp, i32, vp, i32, i32, vp, i32, vp]),
+            "fc_inject": (C.c_int, [G, ST, vp, i32, i32, i32, vp]),
+            "fc_run": (C.c_int, [G, LS, ST, vp, vp, i32, vp, i32, i32, vp, i32, i32, C.POINTER(i32), vp]),
             "fc_contract": (C.c_int, [G, ST, vp, i32, vp, vp, vp]),
             "fc_loss_grad": (C.c_int, [G, ST, vp, i64, vp, i32, vp, vp, vp, vp, vp, vp]),
             "fc_loss_dense": (C.c_int, [i32, i32, vp, vp, vp, vp, vp, vp, vp]),

@@ -35,10 +35,19 @@ def _dev(device) -> torch.device:
     return d
 
 
+def _fast_env(elev, speed, direction, canopy, density) -> torch.Tensor:
+    """fp32 [H][W][4] fast-path record: elevation, wind vector (east, north)
+    = speed * (cos, sin)(direction), and vd = (1 + canopy)(1 + density)."""
+    rad = direction * (np.pi / 180.0)
+    vd = (1.0 + canopy) * (1.0 + density)
+    return torch.stack([elev, speed * torch.cos(rad), speed * torch.sin(rad), vd],
+                       dim=-1).to(torch.float32).contiguous()
+
+
 class DeviceLandscape:
     """Environment rasters in the kernel's layout (see include/firecell.h).
 
-    env fp32 [H][W][4] = (elevation, wind speed, wind direction, vd) feeds the
+    env fp32 [H][W][4] = (elevation, wind east, wind north, vd) feeds the
     fp32 fast path; env64 fp64 [H][W][5] = (elevation, speed, direction,
     canopy, density) feeds the rare fp64 guard recompute; the optional slope
     tensors [H][W][8] replace the elevation-derived slope.
@@ -72,8 +81,7 @@ class DeviceLandscape:
         t64 = [torch.as_tensor(np.asarray(a) if not torch.is_tensor(a) else a).to(dev, torch.float64)
                for a in (elevation, wind_speed, wind_direction, canopy, density)]
         env64 = torch.stack(t64, dim=-1)
-        vd = (1.0 + t64[3]) * (1.0 + t64[4])
-        env = torch.stack([t64[0], t64[1], t64[2], vd], dim=-1).to(torch.float32)
+        env = _fast_env(t64[0], t64[1], t64[2], t64[3], t64[4])
         return cls(env, env64, cell_side=cell_side,
                    slope_sign=-1 if slope_sign == "uphill-positive" else 1,
                    factor_site=factor_site)
@@ -113,8 +121,7 @@ class DeviceLandscape:
         d = torch.as_tensor(np.asarray(wind_direction) if not torch.is_tensor(wind_direction) else wind_direction).to(dev, torch.float64)
         env64 = self.env64.clone()
         env64[..., 1], env64[..., 2] = v, d
-        env = self.env.clone()
-        env[..., 1], env[..., 2] = v.to(torch.float32), d.to(torch.float32)
+        env = _fast_env(env64[..., 0], v, d, env64[..., 3], env64[..., 4])
         out = DeviceLandscape(env, env64, cell_side=self.cell_side, slope32=self.slope32,
                               slope64=self.slope64, slope_sign=self.slope_sign,
                               factor_site=self.factor_site)
@@ -152,7 +159,7 @@ class FireBatch:
         self.h, self.w = int(shape[0]), int(shape[1])
         if self.h < 1 or self.w < 1:
             raise ValueError(f"grid must be at least 1x1, got {shape}")
-        if max_steps >= L.T_NEVER:
+        if max_steps >= L.T_NEVER - 1:
             raise ValueError(f"max_steps must be < {L.T_NEVER}")
         self.m = int(members)
         self.grid = L.grid(self.h, self.w, self.m)
@@ -168,6 +175,7 @@ class FireBatch:
         self.max_steps = int(max_steps)
         self.counters = torch.zeros((self.m, self.max_steps, L.NCOUNTER), dtype=torch.int32,
                                     device=dev)
+        # launches are bounded by steps (>= 1 step per launch) plus resets' lists
         ntiles = self.m * self.grid.tiles_y * self.grid.tiles_x
         self.tile_list = torch.empty((3, ntiles), dtype=torch.int32, device=dev)
         self.list_count = torch.zeros((self.max_steps + 3,), dtype=torch.int32, device=dev)
@@ -177,6 +185,7 @@ class FireBatch:
         ws = max(L.lib().fc_loss_workspace_bytes(C.byref(self.grid), 8), 1 << 12)
         self.workspace = torch.empty((ws,), dtype=torch.uint8, device=dev)
         self.t = 0
+        self.q = 0  # launches since reset (burning-buffer parity, activity lists)
         self.init_burning = np.zeros(self.m, dtype=np.int64)
         self._hw = hw
 
@@ -230,11 +239,13 @@ class FireBatch:
         L.check(L.lib().fc_state_init(C.byref(self.grid), C.byref(st), L.ptr(self._init_mask),
                                       stride, int(t0), L.stream_ptr(stream)), "fc_state_init")
         self.t = int(t0)
+        self.q = 0
 
     def run(self, land: DeviceLandscape, nsteps: int, *, attach: Optional[Sequence[bool]] = None,
             rng: str = "splitmix", draws: Optional[torch.Tensor] = None, skip_inactive: bool = True,
-            stream=None):
-        """Advance every member nsteps steps from the current pre-step index."""
+            window: int = 8, stream=None):
+        """Advance every member nsteps steps from the current pre-step index,
+        `window` steps per kernel launch (temporal blocking; 1, 4, 8, 16)."""
         if nsteps < 0:
             raise ValueError("steps must be >= 0")
         if land.shape != (self.h, self.w):
@@ -252,11 +263,16 @@ class FireBatch:
             if draws is None or tuple(draws.shape) != (nsteps, self.m, 2, self.h, self.w):
                 raise ValueError("inject mode needs draws of shape (nsteps, M, 2, H, W)")
             draws = draws.to(self.device, torch.float64).contiguous()
+        if window not in (1, 4, 8, 16):
+            raise ValueError("window must be 1, 4, 8 or 16")
         lst, st = land.struct(), self.struct()
+        phase = C.c_int32(self.q)
         L.check(L.lib().fc_run(C.byref(self.grid), C.byref(lst), C.byref(st), L.ptr(self.params),
                                L.ptr(self.seeds), mode, L.ptr(draws), self.t, int(nsteps), att,
-                               1 if skip_inactive else 0, L.stream_ptr(stream)), "fc_run")
+                               1 if skip_inactive else 0, int(window), C.byref(phase),
+                               L.stream_ptr(stream)), "fc_run")
         self.t += int(nsteps)
+        self.q = int(phase.value)
         self._keep = (att_np if attach is not None else None, draws)  # lifetime until sync
 
     def inject(self, cells, member: int = 0, stream=None):
@@ -275,7 +291,7 @@ class FireBatch:
         t = torch.tensor(rows, dtype=torch.int32, device=self.device)
         st = self.struct()
         L.check(L.lib().fc_inject(C.byref(self.grid), C.byref(st), L.ptr(t), len(rows), self.t,
-                                  L.stream_ptr(stream)), "fc_inject")
+                                  self.q, L.stream_ptr(stream)), "fc_inject")
         self._inj = t
 
     def unpack(self, stream=None):
@@ -283,7 +299,7 @@ class FireBatch:
         b = torch.empty((self.m, self.h, self.w), dtype=torch.uint8, device=self.device)
         d = torch.empty_like(b)
         st = self.struct()
-        L.check(L.lib().fc_state_unpack(C.byref(self.grid), C.byref(st), self.t, L.ptr(b),
+        L.check(L.lib().fc_state_unpack(C.byref(self.grid), C.byref(st), self.q, L.ptr(b),
                                         L.ptr(d), L.stream_ptr(stream)), "fc_state_unpack")
         return b, d
 
