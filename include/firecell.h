@@ -195,6 +195,10 @@ int fc_build_fields(const fc_grid* g, const fc_landscape* land, const double* pa
 /* ---------------------------------------------------------- diagnostics --- */
 int fc_last_cuda_error(void);
 const char* fc_version(void);
+/* Builds compiled with -DFC_TRACE record per-CTA phase timestamps of the
+ * window kernel into buf ([512][16][4] int64); NULL disables.  No effect in
+ * regular builds. */
+void fc_debug_set_trace(long long* buf);
 
 #ifdef __cplusplus
 }

@@ -13,7 +13,7 @@ import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 REPO = os.path.dirname(HERE)
-SO_PATH = os.path.join(HERE, "libfirecell.so")
+SO_PATH = os.environ.get("FIRECELL_SO") or os.path.join(HERE, "libfirecell.so")  # override: A/B builds
 CU_PATH = os.path.join(HERE, "csrc", "firecell.cu")
 HEADER = os.path.join(REPO, "include", "firecell.h")
 
@@ -32,7 +32,7 @@ NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", 
 EXPORTS = ("fc_grid_make", "fc_plane_words", "fc_loss_workspace_bytes", "fc_state_init",
            "fc_state_unpack", "fc_inject", "fc_run", "fc_contract", "fc_loss_grad",
            "fc_loss_dense", "fc_adamw", "fc_uniform_grid", "fc_epoch_seed", "fc_build_fields",
-           "fc_last_cuda_error", "fc_version")
+           "fc_last_cuda_error", "fc_version", "fc_debug_set_trace")
 
 
 class FcGrid(C.Structure):
@@ -101,8 +101,11 @@ def lib():
             "fc_build_fields": (C.c_int, [G, LS, vp, vp, i32, vp]),
             "fc_last_cuda_error": (C.c_int, []),
             "fc_version": (C.c_char_p, []),
+            "fc_debug_set_trace": (None, [vp]),
         }
         for name, (res, args) in sig.items():
+            if name == "fc_debug_set_trace" and not hasattr(L, name):
+                continue  # diagnostics symbol, absent from older A/B builds
             fn = getattr(L, name)
             fn.restype = res
             fn.argtypes = args

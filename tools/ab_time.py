@@ -1,0 +1,55 @@
+"""Quick A/B timing of builds: FIRECELL_SO=<so> python tools/ab_time.py"""
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2502_18738_b200 as F  # noqa: E402
+from paper_2502_18738_b200 import synthetic as S  # noqa: E402
+
+
+def timeit(fn, reps=5):
+    fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+def main():
+    window = int(os.environ.get("WINDOW", 8))
+    env = S.make_environment(2048, seed=1)
+    dl = F.DeviceLandscape.from_environment(env)
+    b = F.FireBatch((2048, 2048), 16, max_steps=500)
+    ph = S.ensemble_ph(16)
+    b.set_params(np.array([F.pack_params(0.045, 0.131, 0.078, p, 0.3) for p in ph]))
+    b.set_seeds(list(range(16)))
+    init = torch.as_tensor(S.center_ignition(2048).astype(np.uint8), device="cuda")
+
+    def c1():
+        b.reset(init)
+        b.run(dl, 500, window=window)
+    print(os.environ.get("FIRECELL_SO", "default"), "window", window, "c1 ms/run %.3f" % timeit(c1))
+    n = 1024
+    env2 = S.make_environment(n, seed=2)
+    dl2 = F.DeviceLandscape.from_environment(env2)
+    b2 = F.FireBatch((n, n), 1, max_steps=100, with_jacobian=True)
+    b2.set_params(F.pack_params(0.045, 0.131, 0.078, 0.58, 0.3))
+    b2.set_seeds([7])
+    init2 = torch.as_tensor(S.center_ignition(n).astype(np.uint8), device="cuda")
+
+    def c2fwd():
+        b2.reset(init2)
+        b2.run(dl2, 100, attach=[True] * 100, window=window)
+    print("c2 fwd(all attached) ms/iter %.3f" % timeit(c2fwd, 20))
+
+
+if __name__ == "__main__":
+    main()
