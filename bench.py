@@ -312,6 +312,10 @@ def run_ours(args):
            "api": "paper_2502_18738_b200.ensemble.EnsembleRunner (pinned host in/out)"}
 
     extras = {}
+    if not args.no_extras:
+        c4 = bench_ensemble_calibration(dev, rank, world)
+        if rank == 0:
+            extras["ensemble_calibration"] = c4
     if rank == 0 and world == 1 and not args.no_extras:
         extras["calibration"] = bench_calibration(dev)
         extras["dense_probe"] = bench_dense(dev, peak)
@@ -393,6 +397,76 @@ def bench_calibration(dev):
             "loss": "sum over 4 targets of combined_loss (BCE crop + 4x4 pooled MSE)",
             "final_loss": float(loss[0, 0]), "final_params_c1_c2_a_ph_pc": p.tolist(),
             "note": "p_continue gradient is identically 0 under straight-through semantics"}
+
+
+def bench_ensemble_calibration(dev, rank, world, members_total=256, iters=3):
+    """Config 4: 256 members x 1024^2 x 200 steps, all steps attached, wind
+    rotating +90 deg and ramping 2 -> 12 m/s (device schedule), per-member
+    4-target loss + gradient, gradients summed over members and all-reduced
+    over ranks (NCCL), one AdamW step on the shared parameters.  Members are
+    sharded by rank; iteration time is the max over ranks."""
+    import torch
+
+    import paper_2502_18738_b200 as F
+    from paper_2502_18738_b200 import synthetic as S
+    from paper_2502_18738_b200.device import wind_ramp_schedule
+    from paper_2502_18738_b200.parallel import allreduce_max, allreduce_sum_, shard_members
+    n, T = 1024, 200
+    env = S.make_environment(n, seed=4)
+    dl = F.DeviceLandscape.from_environment(env, device=dev)
+    sched = wind_ramp_schedule(T, 2.0, 12.0, 90.0, device=dev)
+    init = torch.as_tensor(S.center_ignition(n).astype(np.uint8), device=dev)
+    hid = S.HIDDEN_C2_PARAMS
+    tb = F.FireBatch((n, n), 1, max_steps=T, device=dev)
+    tb.set_params(F.pack_params(hid["c1"], hid["c2"], hid["a"], hid["p_h"], hid["p_continue"]))
+    tb.set_seeds([7])
+    tb.reset(init)
+    obs = [50, 100, 150, 200]
+    targets = []
+    for k in range(4):
+        tb.run(dl, 50, wind_schedule=sched)
+        b_, d_ = tb.unpack()
+        targets.append(b_[0] | d_[0])
+    targets = torch.stack(targets)
+    del tb
+    mine = shard_members(members_total, rank, world)
+    b = F.FireBatch((n, n), len(mine), max_steps=T, with_jacobian=True, device=dev)
+    p0 = S.DEFAULT_BENCH_PARAMS
+    b.set_params(F.pack_params(p0["c1"], p0["c2"], p0["a"], p0["p_h"], p0["p_continue"]))
+    b.set_seeds(mine)
+    attach = [True] * T
+    shared = torch.zeros((1, 8), dtype=torch.float64, device=dev)
+    shared.copy_(b.params[:1])
+    adam = torch.zeros((1, 8), dtype=torch.float64, device=dev)
+    from paper_2502_18738_b200 import _lib as L
+
+    def iteration(k):
+        b.params.copy_(shared.expand_as(b.params))
+        b.reset(init)
+        b.run(dl, T, attach=attach, wind_schedule=sched)
+        loss, _, grad, _ = b.loss_grad(targets, obs)
+        g = grad.sum(0, keepdim=True)
+        allreduce_sum_(g)
+        L.check(L.lib().fc_adamw(g.data_ptr(), shared.data_ptr(), adam.data_ptr(), 1, k, 1e-2, 0.0,
+                                 0.9, 0.999, 1e-8, 1, 0, L.stream_ptr()), "fc_adamw")
+        return loss
+
+    iteration(1)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for k in range(2, 2 + iters):
+        loss = iteration(k)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = allreduce_max(e0.elapsed_time(e1) / iters, dev)
+    return {"iter_per_s": 1e3 / ms, "ms_per_iter": ms, "members": members_total,
+            "members_per_rank": len(mine), "grid": [n, n], "steps": T, "attached": "all",
+            "fwd_bwd_cell_updates_per_s": members_total * n * n * T / (ms / 1e3),
+            "wind": "direction +90 deg linear, speed 2->12 m/s linear (device schedule)",
+            "targets": "hidden-parameter run (seed 7) affected masks at 50/100/150/200",
+            "mean_member_loss": float(loss[:, 0].mean()),
+            "params_after_c1_c2_a_ph": shared[0, :4].cpu().numpy().tolist()}
 
 
 def bench_dense(dev, peak):

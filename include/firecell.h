@@ -79,6 +79,8 @@ typedef struct {
     const double* env64;    /* [H][W][5] fp64                           */
     const float* slope32;   /* [H][W][8] fp32, FC_SLOPE_TENSOR only     */
     const double* slope64;  /* [H][W][8] fp64, FC_SLOPE_TENSOR only     */
+    const float* dir32;     /* [H][W][2] fp32 (cos, sin) of the wind direction; needed by
+                               per-step wind schedules                   */
     double cell_side;       /* metres (kernel uses l and l*sqrt(2))     */
     int32_t slope_mode;     /* FC_SLOPE_*                                */
     int32_t slope_sign;     /* +1 downhill-positive, -1 uphill-positive */
@@ -134,11 +136,16 @@ int fc_inject(const fc_grid* g, const fc_state* s, const int32_t* cells, int32_t
  * skip_inactive: 1 = only tiles near burning cells are visited (exact: the
  * analogue of the reference's bounding-box window, kernel.py:296-302).
  * window: steps fused per launch (temporal blocking; 1, 4, 8 or 16).
+ * wind_schedule: NULL, or fp64 [max_steps][4] = {alpha, beta, gamma_deg, 0}
+ * indexed by pre-step index: step t sees speed alpha*V + beta and direction
+ * theta + gamma (a WindUpdate, kernel.py:422-428/505-511, for every step
+ * without re-uploading fields; config 4's rotating, ramping wind).
  * host_phase: in/out launch counter (see fc_state_unpack). */
 int fc_run(const fc_grid* g, const fc_landscape* land, const fc_state* s,
            const double* params, const uint64_t* seeds, int32_t rng_mode,
            const double* draws, int32_t t0, int32_t nsteps, const uint8_t* host_attach,
-           int32_t skip_inactive, int32_t window, int32_t* host_phase, fc_stream_t stream);
+           int32_t skip_inactive, int32_t window, const double* wind_schedule,
+           int32_t* host_phase, fc_stream_t stream);
 
 /* ----------------------------------------------------------- backward --- */
 /* backward_params (tape.py:118-148): out[m][4] = sum_j g[m][j] * J[m][j] in

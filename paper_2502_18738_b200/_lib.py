@@ -42,7 +42,8 @@ class FcGrid(C.Structure):
 
 class FcLandscape(C.Structure):
     _fields_ = [("env", C.c_void_p), ("env64", C.c_void_p), ("slope32", C.c_void_p),
-                ("slope64", C.c_void_p), ("cell_side", C.c_double), ("slope_mode", C.c_int32),
+                ("slope64", C.c_void_p), ("dir32", C.c_void_p), ("cell_side", C.c_double),
+                ("slope_mode", C.c_int32),
                 ("slope_sign", C.c_int32), ("factor_source", C.c_int32), ("pad_", C.c_int32)]
 
 
@@ -91,7 +92,8 @@ def lib():
             "fc_state_init": (C.c_int, [G, ST, vp, i64, i32, vp]),
             "fc_state_unpack": (C.c_int, [G, ST, i32, vp, vp, vp]),
             "fc_inject": (C.c_int, [G, ST, vp, i32, i32, i32, vp]),
-            "fc_run": (C.c_int, [G, LS, ST, vp, vp, i32, vp, i32, i32, vp, i32, i32, C.POINTER(i32), vp]),
+            "fc_run": (C.c_int, [G, LS, ST, vp, vp, i32, vp, i32, i32, vp, i32, i32, vp,
+                                 C.POINTER(i32), vp]),
             "fc_contract": (C.c_int, [G, ST, vp, i32, vp, vp, vp]),
             "fc_loss_grad": (C.c_int, [G, ST, vp, i64, vp, i32, vp, vp, vp, vp, vp, vp]),
             "fc_loss_dense": (C.c_int, [i32, i32, vp, vp, vp, vp, vp, vp, vp]),

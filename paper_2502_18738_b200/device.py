@@ -59,6 +59,8 @@ class DeviceLandscape:
         if factor_site not in ("target", "source"):
             raise ValueError(f"factor_site must be 'target' or 'source', got {factor_site!r}")
         self.env, self.env64 = env.contiguous(), env64.contiguous()
+        rad = self.env64[..., 2] * (np.pi / 180.0)
+        self.dir32 = torch.stack([torch.cos(rad), torch.sin(rad)], dim=-1).to(torch.float32).contiguous()
         self.slope32 = None if slope32 is None else slope32.contiguous()
         self.slope64 = None if slope64 is None else slope64.contiguous()
         self.cell_side = float(cell_side)
@@ -131,6 +133,7 @@ class DeviceLandscape:
         s = L.FcLandscape()
         s.env, s.env64 = L.ptr(self.env), L.ptr(self.env64)
         s.slope32, s.slope64 = L.ptr(self.slope32), L.ptr(self.slope64)
+        s.dir32 = L.ptr(self.dir32)
         s.cell_side = self.cell_side
         s.slope_mode = L.SLOPE_TENSOR if self.slope64 is not None else L.SLOPE_ELEVATION
         s.slope_sign = self.slope_sign
@@ -141,6 +144,31 @@ class DeviceLandscape:
     def nbytes(self) -> int:
         return sum(t.numel() * t.element_size() for t in
                    (self.env, self.env64, self.slope32, self.slope64) if t is not None)
+
+
+def wind_ramp_schedule(steps: int, v_start: float = 2.0, v_end: float = 12.0,
+                       rotate_deg: float = 90.0, keep_field: bool = False,
+                       device=None) -> torch.Tensor:
+    """Per-step wind schedule of BASELINE config 4: the direction rotates
+    linearly by rotate_deg over the run and the speed ramps linearly from
+    v_start to v_end (uniform speed; keep_field=True scales the base field
+    instead).  Row t = {alpha, beta, gamma_deg, 0} for pre-step index t."""
+    frac = np.arange(steps, dtype=np.float64) / max(steps - 1, 1)
+    speed = v_start + (v_end - v_start) * frac
+    sched = np.zeros((steps, 4), dtype=np.float64)
+    if keep_field:
+        sched[:, 0] = speed / max(v_start, 1e-12)
+    else:
+        sched[:, 1] = speed
+    sched[:, 2] = rotate_deg * frac
+    return torch.as_tensor(sched, device=device if device is not None else "cuda")
+
+
+def scheduled_wind_fields(speed, direction, row):
+    """fp64 host fields one schedule row implies (for the reference API /
+    oracle): speed' = alpha * speed + beta, direction' = direction + gamma."""
+    a, b, g = float(row[0]), float(row[1]), float(row[2])
+    return a * np.asarray(speed, dtype=np.float64) + b, np.asarray(direction, dtype=np.float64) + g
 
 
 def pack_params(c1, c2, a, p_h, p_continue, norm_c=DEFAULT_NORM_C) -> list:
@@ -243,9 +271,11 @@ class FireBatch:
 
     def run(self, land: DeviceLandscape, nsteps: int, *, attach: Optional[Sequence[bool]] = None,
             rng: str = "splitmix", draws: Optional[torch.Tensor] = None, skip_inactive: bool = True,
-            window: int = 8, stream=None):
+            window: int = 8, wind_schedule: Optional[torch.Tensor] = None, stream=None):
         """Advance every member nsteps steps from the current pre-step index,
-        `window` steps per kernel launch (temporal blocking; 1, 4, 8, 16)."""
+        `window` steps per kernel launch (temporal blocking; 1, 4, 8, 16).
+        wind_schedule: optional fp64 (max_steps, 4) device tensor of per-step
+        {alpha, beta, gamma_deg, 0} (see wind_ramp_schedule)."""
         if nsteps < 0:
             raise ValueError("steps must be >= 0")
         if land.shape != (self.h, self.w):
@@ -265,12 +295,16 @@ class FireBatch:
             draws = draws.to(self.device, torch.float64).contiguous()
         if window not in (1, 4, 8, 16):
             raise ValueError("window must be 1, 4, 8 or 16")
+        if wind_schedule is not None:
+            if tuple(wind_schedule.shape) != (self.max_steps, 4) or wind_schedule.dtype != torch.float64:
+                raise ValueError("wind_schedule must be fp64 of shape (max_steps, 4)")
+            wind_schedule = wind_schedule.to(self.device).contiguous()
         lst, st = land.struct(), self.struct()
         phase = C.c_int32(self.q)
         L.check(L.lib().fc_run(C.byref(self.grid), C.byref(lst), C.byref(st), L.ptr(self.params),
                                L.ptr(self.seeds), mode, L.ptr(draws), self.t, int(nsteps), att,
-                               1 if skip_inactive else 0, int(window), C.byref(phase),
-                               L.stream_ptr(stream)), "fc_run")
+                               1 if skip_inactive else 0, int(window), L.ptr(wind_schedule),
+                               C.byref(phase), L.stream_ptr(stream)), "fc_run")
         self.t += int(nsteps)
         self.q = int(phase.value)
         self._keep = (att_np if attach is not None else None, draws)  # lifetime until sync

@@ -329,3 +329,36 @@ def test_temporal_blocking_and_sweep_modes_bit_identical(attach):
         if attach:
             assert torch.equal(base[4], other[4])
         assert np.array_equal(base[5], other[5])
+
+
+def test_scheduled_wind_matches_oracle_with_per_step_updates():
+    """Config-4 style per-step wind schedule (rotating direction, ramping
+    speed) against the oracle fed one WindUpdate per step (kernel.py:505-511)."""
+    from paper_2502_18738_b200.device import scheduled_wind_fields, wind_ramp_schedule
+    h, w, steps = 96, 80, 40
+    env = S.make_environment(h, w, seed=21)
+    dl = F.DeviceLandscape.from_environment(env)
+    sched = wind_ramp_schedule(steps, 2.0, 12.0, 90.0)
+    b = F.FireBatch((h, w), 2, max_steps=steps, with_jacobian=True)
+    b.set_params(F.pack_params(0.05, 0.1, 0.07, 0.5, 0.4))
+    b.set_seeds([3, 4])
+    init = S.center_ignition(h, w)
+    b.reset(init)
+    b.run(dl, steps, attach=[True] * steps, wind_schedule=sched, window=8)
+    arr = S.reference_landscape_arrays(env, O.slope_from_altitude)
+    rows = sched.cpu().numpy()
+    updates = []
+    for t in range(steps):
+        v, d = scheduled_wind_fields(arr["wind_speed"], arr["wind_direction"], rows[t])
+        updates.append((t + 1, v, d))
+    bu, bd = (x.bool().cpu().numpy() for x in b.unpack())
+    tg = np.zeros((h, w), bool)
+    tg[30:70, 20:60] = True
+    _, _, g_dev, _ = b.loss_grad(torch.as_tensor(tg), [steps])
+    for m in range(2):
+        res = O.run(**arr, params=P([0.05, 0.1, 0.07, 0.5, 0.4]), init=init, steps=steps,
+                    seed=3 + m, attach_steps=range(1, steps + 1), wind_schedule=updates)
+        assert np.array_equal(bu[m], res.burning) and np.array_equal(bd[m], res.burned)
+        np.testing.assert_allclose(b.acc[m].double().cpu().numpy(), res.acc, rtol=RTOL_ACC)
+        _, _, _, g = O.combined_loss(res.acc, tg)
+        np.testing.assert_allclose(g_dev[m].cpu().numpy(), O.contract(res.jac, g), rtol=RTOL_GRAD)
