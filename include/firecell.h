@@ -103,6 +103,17 @@ typedef struct {
     int32_t pad_;
 } fc_state;
 
+/* Row-sharded single domain (BASELINE config 3 across GPUs): the local grid
+ * holds this rank's rows plus ghost tile rows (32 rows each) copied from the
+ * neighbouring ranks after every launch.  Ghost tiles are read as halo and
+ * never advanced; draws are keyed by the global row = local row + row0. */
+typedef struct {
+    int32_t row0;           /* global row of local row 0                    */
+    int32_t ghost_top;      /* ghost tile rows at the top (0 or 1)          */
+    int32_t ghost_bottom;   /* ghost tile rows at the bottom (0 or 1)       */
+    int32_t pad_;
+} fc_shard;
+
 /* ------------------------------------------------------------ sizing --- */
 void fc_grid_make(int32_t height, int32_t width, int32_t members, fc_grid* out);
 size_t fc_plane_words(const fc_grid* g);              /* uint32 words per plane   */
@@ -140,12 +151,19 @@ int fc_inject(const fc_grid* g, const fc_state* s, const int32_t* cells, int32_t
  * indexed by pre-step index: step t sees speed alpha*V + beta and direction
  * theta + gamma (a WindUpdate, kernel.py:422-428/505-511, for every step
  * without re-uploading fields; config 4's rotating, ramping wind).
+ * shard: NULL, or the row-shard descriptor (ghost rows are not advanced).
  * host_phase: in/out launch counter (see fc_state_unpack). */
 int fc_run(const fc_grid* g, const fc_landscape* land, const fc_state* s,
            const double* params, const uint64_t* seeds, int32_t rng_mode,
            const double* draws, int32_t t0, int32_t nsteps, const uint8_t* host_attach,
            int32_t skip_inactive, int32_t window, const double* wind_schedule,
-           int32_t* host_phase, fc_stream_t stream);
+           const fc_shard* shard, int32_t* host_phase, fc_stream_t stream);
+
+/* After the ghost rows were refreshed with the neighbours' state at launch
+ * phase `phase`, activate the owned tiles next to ghost tiles holding fire
+ * (the marks a neighbour's tiles would have made in an unsharded run). */
+int fc_mark_ghosts(const fc_grid* g, const fc_state* s, const fc_shard* shard, int32_t phase,
+                   fc_stream_t stream);
 
 /* ----------------------------------------------------------- backward --- */
 /* backward_params (tape.py:118-148): out[m][4] = sum_j g[m][j] * J[m][j] in

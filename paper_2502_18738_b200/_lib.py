@@ -30,7 +30,7 @@ NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", 
 
 # Every symbol include/firecell.h declares (checked by the CPU test suite).
 EXPORTS = ("fc_grid_make", "fc_plane_words", "fc_loss_workspace_bytes", "fc_state_init",
-           "fc_state_unpack", "fc_inject", "fc_run", "fc_contract", "fc_loss_grad",
+           "fc_state_unpack", "fc_inject", "fc_run", "fc_mark_ghosts", "fc_contract", "fc_loss_grad",
            "fc_loss_dense", "fc_adamw", "fc_uniform_grid", "fc_epoch_seed", "fc_build_fields",
            "fc_last_cuda_error", "fc_version", "fc_debug_set_trace")
 
@@ -45,6 +45,11 @@ class FcLandscape(C.Structure):
                 ("slope64", C.c_void_p), ("dir32", C.c_void_p), ("cell_side", C.c_double),
                 ("slope_mode", C.c_int32),
                 ("slope_sign", C.c_int32), ("factor_source", C.c_int32), ("pad_", C.c_int32)]
+
+
+class FcShard(C.Structure):
+    _fields_ = [("row0", C.c_int32), ("ghost_top", C.c_int32), ("ghost_bottom", C.c_int32),
+                ("pad_", C.c_int32)]
 
 
 class FcState(C.Structure):
@@ -85,6 +90,7 @@ def lib():
         L = C.CDLL(SO_PATH)
         vp, i32, i64, u64, dbl = C.c_void_p, C.c_int32, C.c_int64, C.c_uint64, C.c_double
         G, LS, ST = C.POINTER(FcGrid), C.POINTER(FcLandscape), C.POINTER(FcState)
+        SH = C.POINTER(FcShard)
         sig = {
             "fc_grid_make": (None, [i32, i32, i32, G]),
             "fc_plane_words": (C.c_size_t, [G]),
@@ -92,8 +98,9 @@ def lib():
             "fc_state_init": (C.c_int, [G, ST, vp, i64, i32, vp]),
             "fc_state_unpack": (C.c_int, [G, ST, i32, vp, vp, vp]),
             "fc_inject": (C.c_int, [G, ST, vp, i32, i32, i32, vp]),
-            "fc_run": (C.c_int, [G, LS, ST, vp, vp, i32, vp, i32, i32, vp, i32, i32, vp,
+            "fc_run": (C.c_int, [G, LS, ST, vp, vp, i32, vp, i32, i32, vp, i32, i32, vp, SH,
                                  C.POINTER(i32), vp]),
+            "fc_mark_ghosts": (C.c_int, [G, ST, SH, i32, vp]),
             "fc_contract": (C.c_int, [G, ST, vp, i32, vp, vp, vp]),
             "fc_loss_grad": (C.c_int, [G, ST, vp, i64, vp, i32, vp, vp, vp, vp, vp, vp]),
             "fc_loss_dense": (C.c_int, [i32, i32, vp, vp, vp, vp, vp, vp, vp]),

@@ -271,7 +271,8 @@ class FireBatch:
 
     def run(self, land: DeviceLandscape, nsteps: int, *, attach: Optional[Sequence[bool]] = None,
             rng: str = "splitmix", draws: Optional[torch.Tensor] = None, skip_inactive: bool = True,
-            window: int = 8, wind_schedule: Optional[torch.Tensor] = None, stream=None):
+            window: int = 8, wind_schedule: Optional[torch.Tensor] = None, shard=None,
+            stream=None):
         """Advance every member nsteps steps from the current pre-step index,
         `window` steps per kernel launch (temporal blocking; 1, 4, 8, 16).
         wind_schedule: optional fp64 (max_steps, 4) device tensor of per-step
@@ -304,7 +305,8 @@ class FireBatch:
         L.check(L.lib().fc_run(C.byref(self.grid), C.byref(lst), C.byref(st), L.ptr(self.params),
                                L.ptr(self.seeds), mode, L.ptr(draws), self.t, int(nsteps), att,
                                1 if skip_inactive else 0, int(window), L.ptr(wind_schedule),
-                               C.byref(phase), L.stream_ptr(stream)), "fc_run")
+                               None if shard is None else C.byref(shard), C.byref(phase),
+                               L.stream_ptr(stream)), "fc_run")
         self.t += int(nsteps)
         self.q = int(phase.value)
         self._keep = (att_np if attach is not None else None, draws)  # lifetime until sync
