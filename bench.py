@@ -314,8 +314,10 @@ def run_ours(args):
     extras = {}
     if not args.no_extras:
         c4 = bench_ensemble_calibration(dev, rank, world)
+        c3 = bench_row_sharded(dev, rank, world)
         if rank == 0:
             extras["ensemble_calibration"] = c4
+            extras["row_sharded"] = c3
     if rank == 0 and world == 1 and not args.no_extras:
         extras["calibration"] = bench_calibration(dev)
         extras["dense_probe"] = bench_dense(dev, peak)
@@ -467,6 +469,44 @@ def bench_ensemble_calibration(dev, rank, world, members_total=256, iters=3):
             "targets": "hidden-parameter run (seed 7) affected masks at 50/100/150/200",
             "mean_member_loss": float(loss[:, 0].mean()),
             "params_after_c1_c2_a_ph": shared[0, :4].cpu().numpy().tolist()}
+
+
+def bench_row_sharded(dev, rank, world, steps=200, window=8):
+    """Config 3 layout across ranks (weak scaling): each rank owns 2048 rows
+    of a (2048*world) x 16384 domain (sigma x32 env generated on the device,
+    2 random 5x5 ignitions per rank band); K-row halos of both bit planes are
+    exchanged over NCCL after every window launch.  Device time, max over
+    ranks; value = global cell-updates/s."""
+    import torch
+
+    from paper_2502_18738_b200 import synthetic as S
+    from paper_2502_18738_b200.parallel import allreduce_max, barrier
+    from paper_2502_18738_b200.sharded import RowPartition, RowShard, run_sharded
+    import paper_2502_18738_b200 as F
+    H, Wd = 2048 * world, 16384
+    e = S.make_environment_torch(H, Wd, seed=3, sigma_elev=640.0, sigma_wind=960.0, device=dev)
+    init = torch.as_tensor(S.random_blocks(H, Wd, 2 * world, 5, seed=3).astype(np.uint8),
+                           device=dev)
+    part = RowPartition(H, world, rank)
+    sh = RowShard(part, e["elevation"], e["wind_speed"], e["wind_direction"], e["canopy"],
+                  e["density"], init, max_steps=steps, device=dev)
+    del e
+    sh.batch.set_params(F.pack_params(0.045, 0.131, 0.078, 0.58, 0.3))
+    sh.batch.set_seeds([3])
+    run_sharded(sh, 2 * window, window)  # warm-up (NCCL communicators, caches)
+    sh.batch.reset(sh.batch._init_mask)
+    torch.cuda.synchronize()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    run_sharded(sh, steps, window)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = allreduce_max(e0.elapsed_time(e1), dev)
+    return {"grid": [H, Wd], "rows_per_rank": 2048, "ranks": world, "steps": steps,
+            "steps_per_launch": window, "cell_updates_per_s": H * Wd * steps / (ms / 1e3),
+            "ms": ms, "halo": "2 bit planes x 1 tile row (32 rows) each way per window, NCCL P2P",
+            "scaling": "weak"}
 
 
 def bench_dense(dev, peak):
