@@ -320,6 +320,7 @@ def run_ours(args):
             extras["row_sharded"] = c3
     if rank == 0 and world == 1 and not args.no_extras:
         extras["calibration"] = bench_calibration(dev)
+        extras["fig6_sweep"] = bench_fig6_sweep(dev)
         extras["dense_probe"] = bench_dense(dev, peak)
     cpu = None
     if rank == 0 and world == 1:
@@ -373,28 +374,39 @@ def bench_calibration(dev):
     b.set_seeds([F.derive_epoch_seed(7, 1)])
     attach = [True] * T
 
-    def iteration(k):
+    out = {}
+
+    def iteration():
         b.reset(init)
         b.run(dl, T, attach=attach)
-        _, _, grad, _ = b.loss_grad(targets, obs)
-        b.adamw(grad, k, 1e-2)
-        return grad
+        out["loss"], _, out["grad"], _ = b.loss_grad(targets, obs)
+        b.adamw(out["grad"], None, 1e-2)  # device step counter: graph-replayable
 
-    for k in range(1, 4):
-        iteration(k)
-    b.adam.zero_()
-    b.set_params(F.pack_params(p0["c1"], p0["c2"], p0["a"], p0["p_h"], p0["p_continue"]))
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for k in range(1, iters + 1):
-        iteration(k)
-    e1.record()
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1)
-    loss, _, grad, _ = b.loss_grad(targets, obs)
+    def restart():
+        b.adam.zero_()
+        b.adam_step.zero_()
+        b.set_params(F.pack_params(p0["c1"], p0["c2"], p0["a"], p0["p_h"], p0["p_continue"]))
+
+    def timed(fn):
+        restart()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(iters):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1)
+
+    for _ in range(3):
+        iteration()
+    ms_plain = timed(iteration)
+    graph = F.CapturedSequence(iteration)
+    ms = timed(graph.replay)  # one CUDA graph per iteration (reset + windows + loss + AdamW)
+    loss, grad = out["loss"], out["grad"]
     p = b.params[0, :5].cpu().numpy()
     return {"iter_per_s": iters / (ms / 1e3), "ms_per_iter": ms / iters, "iterations": iters,
+            "iter_per_s_without_graph": iters / (ms_plain / 1e3),
             "grid": [n, n], "steps_per_iter": T, "attached": "all 100 steps",
             "loss": "sum over 4 targets of combined_loss (BCE crop + 4x4 pooled MSE)",
             "final_loss": float(loss[0, 0]), "final_params_c1_c2_a_ph_pc": p.tolist(),
@@ -449,8 +461,8 @@ def bench_ensemble_calibration(dev, rank, world, members_total=256, iters=3):
         loss, _, grad, _ = b.loss_grad(targets, obs)
         g = grad.sum(0, keepdim=True)
         allreduce_sum_(g)
-        L.check(L.lib().fc_adamw(g.data_ptr(), shared.data_ptr(), adam.data_ptr(), 1, k, 1e-2, 0.0,
-                                 0.9, 0.999, 1e-8, 1, 0, L.stream_ptr()), "fc_adamw")
+        L.check(L.lib().fc_adamw(g.data_ptr(), shared.data_ptr(), adam.data_ptr(), 1, k, None,
+                                 1e-2, 0.0, 0.9, 0.999, 1e-8, 1, None, L.stream_ptr()), "fc_adamw")
         return loss
 
     iteration(1)
@@ -507,6 +519,43 @@ def bench_row_sharded(dev, rank, world, steps=200, window=8):
             "steps_per_launch": window, "cell_updates_per_s": H * Wd * steps / (ms / 1e3),
             "ms": ms, "halo": "2 bit planes x 1 tile row (32 rows) each way per window, NCCL P2P",
             "scaling": "weak"}
+
+
+def bench_fig6_sweep(dev, sizes=(200, 1000, 2000, 4000, 8000, 14000), steps=300):
+    """The paper's Fig.-6 style scaling sweep (the
+    reference CLI bench, pyrocell/cli.py:241-287): flat landscape, V_w = 2,
+    default ModelParams (p_continue 0.5), centre ignition, 300 steps.
+    'device_s' = kernel time of the run; 'wall_s' = landscape build + state
+    allocation + run + final state copied to host."""
+    import torch
+
+    import paper_2502_18738_b200 as F
+    from paper_2502_18738_b200 import synthetic as S
+    rows = []
+    for n in sizes:
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        z = torch.zeros((n, n), dtype=torch.float32, device=dev)
+        dl = F.DeviceLandscape.from_elevation(z, torch.full_like(z, 2.0), z, z, z, device=dev)
+        b = F.FireBatch((n, n), 1, max_steps=steps, device=dev)
+        b.set_params(F.pack_params(0.045, 0.131, 0.078, 0.58, 0.5))
+        b.set_seeds([0])
+        b.reset(torch.as_tensor(S.center_ignition(n).astype(np.uint8), device=dev))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        b.run(dl, steps, window=WINDOW)
+        e1.record()
+        bu, bd = b.unpack()
+        host = (bu.cpu(), bd.cpu(), b.acc.cpu())
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        rows.append({"size": n, "device_s": e0.elapsed_time(e1) / 1e3, "wall_s": wall,
+                     "affected": int(host[0].sum() + host[1].sum())})
+        del dl, b, z, host
+        torch.cuda.empty_cache()
+    return {"steps": steps, "rows": rows,
+            "paper": "PyTorchFire: <1 s for maps <1200 (RTX 4090), <=1500 (A800); <60 s at 14000 "
+                     "on 'a more advanced GPU'; CPU 300 steps at 1000^2 ~30 s (PAPER.md:456-467)"}
 
 
 def bench_dense(dev, peak):

@@ -197,11 +197,12 @@ int fc_loss_dense(int32_t height, int32_t width, const double* acc, const uint8_
 
 /* adamw_update + clamp_params (calibration.py:43-64, model.py:47-57) on the
  * device params [M][8] with per-member moments adam[M][8] = {m[4], v[4]}.
- * step = 1-based Adam step.  A non-finite gradient leaves that member's
- * params untouched and sets status[m] = 1 (else 0). */
+ * step = 1-based Adam step, or dev_step (device int32 [M], incremented by the
+ * kernel) for CUDA-graph replays.  A non-finite gradient leaves that member's
+ * params and step untouched and sets status[m] = 1 (else 0). */
 int fc_adamw(const double* grads, double* params, double* adam, int32_t members,
-             int32_t step, double lr, double weight_decay, double beta1, double beta2,
-             double eps, int32_t clamp, int32_t* status, fc_stream_t stream);
+             int32_t step, int32_t* dev_step, double lr, double weight_decay, double beta1,
+             double beta2, double eps, int32_t clamp, int32_t* status, fc_stream_t stream);
 
 /* ---------------------------------------------------------------- rng --- */
 /* uniform_grid (rng.py:55-75) on the device: out [height][width] fp64. */

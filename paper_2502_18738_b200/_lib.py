@@ -104,7 +104,7 @@ def lib():
             "fc_contract": (C.c_int, [G, ST, vp, i32, vp, vp, vp]),
             "fc_loss_grad": (C.c_int, [G, ST, vp, i64, vp, i32, vp, vp, vp, vp, vp, vp]),
             "fc_loss_dense": (C.c_int, [i32, i32, vp, vp, vp, vp, vp, vp, vp]),
-            "fc_adamw": (C.c_int, [vp, vp, vp, i32, i32, dbl, dbl, dbl, dbl, dbl, i32, vp, vp]),
+            "fc_adamw": (C.c_int, [vp, vp, vp, i32, i32, vp, dbl, dbl, dbl, dbl, dbl, i32, vp, vp]),
             "fc_uniform_grid": (C.c_int, [u64, i64, i32, i64, i64, i64, i64, vp, vp]),
             "fc_epoch_seed": (u64, [u64, u64]),
             "fc_build_fields": (C.c_int, [G, LS, vp, vp, i32, vp]),

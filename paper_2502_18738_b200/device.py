@@ -210,6 +210,8 @@ class FireBatch:
         self.params = torch.zeros((self.m, L.NPARAM), dtype=torch.float64, device=dev)
         self.seeds = torch.zeros((self.m,), dtype=torch.int64, device=dev)
         self.adam = torch.zeros((self.m, 8), dtype=torch.float64, device=dev)
+        self.adam_step = torch.zeros((self.m,), dtype=torch.int32, device=dev)
+        self._status = torch.zeros((self.m,), dtype=torch.int32, device=dev)
         ws = max(L.lib().fc_loss_workspace_bytes(C.byref(self.grid), 8), 1 << 12)
         self.workspace = torch.empty((ws,), dtype=torch.uint8, device=dev)
         self.t = 0
@@ -402,11 +404,15 @@ class FireBatch:
         self._keep_t = tg
         return loss, crop, grad, dl
 
-    def adamw(self, grads: torch.Tensor, step: int, lr: float, weight_decay: float = 0.0,
+    def adamw(self, grads: torch.Tensor, step: Optional[int], lr: float, weight_decay: float = 0.0,
               beta1=0.9, beta2=0.999, eps=1e-8, clamp=True, stream=None) -> torch.Tensor:
-        status = torch.zeros((self.m,), dtype=torch.int32, device=self.device)
+        """AdamW + clamp on the device params; step=None uses the device step
+        counter (self.adam_step), which keeps CUDA-graph replays valid."""
+        status = self._status
         L.check(L.lib().fc_adamw(L.ptr(grads), L.ptr(self.params), L.ptr(self.adam), self.m,
-                                 int(step), lr, weight_decay, beta1, beta2, eps, 1 if clamp else 0,
+                                 0 if step is None else int(step),
+                                 L.ptr(self.adam_step) if step is None else None, lr,
+                                 weight_decay, beta1, beta2, eps, 1 if clamp else 0,
                                  L.ptr(status), L.stream_ptr(stream)), "fc_adamw")
         return status
 
@@ -451,3 +457,23 @@ def build_fields_device(land: DeviceLandscape, params8, with_gradients=False, st
                                     1 if with_gradients else 0, L.stream_ptr(stream)),
             "fc_build_fields")
     return out
+
+
+class CapturedSequence:
+    """A CUDA graph of a device-only call sequence (e.g. one calibration
+    iteration: reset + K-step windows + fused loss/gradient + AdamW).  Params,
+    seeds and the Adam step live in device memory, so replays see updates."""
+
+    def __init__(self, fn, warmup: int = 1):
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            for _ in range(warmup):
+                fn()
+        torch.cuda.current_stream().wait_stream(s)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            fn()
+
+    def replay(self):
+        self.graph.replay()

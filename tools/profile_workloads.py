@@ -53,7 +53,7 @@ def main():
             b.reset(S.center_ignition(1024))
             b.run(dl, 100, attach=[True] * 100)
             _, _, g, _ = b.loss_grad(tg, [25, 50, 75, 100])
-            b.adamw(g, k, 1e-2)
+            b.adamw(g, None, 1e-2)
     torch.cuda.synchronize()
     print("done", mode)
 
