@@ -36,7 +36,7 @@
  *   activity      flags int32 [M][TY][TX] = last pre-step index at which the
  *                 tile must be visited; tile_list int32 [3][M*TY*TX] rotating
  *                 compacted lists of tiles active at steps t, t+1, t+2 with
- *                 list_count int32 [max_steps+3] (zeroed by fc_state_init).
+ *                 list_count int32 [2][max_steps+3] (zeroed by fc_state_init).
  *   params        fp64 [M][8] = {c1, c2, a, p_h, p_continue, norm_c, 0, 0}.
  */
 #ifndef FIRECELL_H
@@ -98,7 +98,8 @@ typedef struct {
     int32_t* flags;         /* [M][TY][TX] last pre-step index active   */
     int32_t* counters;      /* [M][max_steps][FC_NCOUNTER]              */
     int32_t* tile_list;     /* [3][M*TY*TX] rotating active-tile lists  */
-    int32_t* list_count;    /* [max_steps+3] length of each step's list */
+    int32_t* list_count;    /* [2][max_steps+3]: list length, then work-
+                               distribution counter, of each launch     */
     int32_t max_steps;
     int32_t pad_;
 } fc_state;

@@ -206,7 +206,7 @@ class FireBatch:
         # launches are bounded by steps (>= 1 step per launch) plus resets' lists
         ntiles = self.m * self.grid.tiles_y * self.grid.tiles_x
         self.tile_list = torch.empty((3, ntiles), dtype=torch.int32, device=dev)
-        self.list_count = torch.zeros((self.max_steps + 3,), dtype=torch.int32, device=dev)
+        self.list_count = torch.zeros((2 * (self.max_steps + 3),), dtype=torch.int32, device=dev)
         self.params = torch.zeros((self.m, L.NPARAM), dtype=torch.float64, device=dev)
         self.seeds = torch.zeros((self.m,), dtype=torch.int64, device=dev)
         self.adam = torch.zeros((self.m, 8), dtype=torch.float64, device=dev)
