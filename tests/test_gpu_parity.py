@@ -362,3 +362,86 @@ def test_scheduled_wind_matches_oracle_with_per_step_updates():
         np.testing.assert_allclose(b.acc[m].double().cpu().numpy(), res.acc, rtol=RTOL_ACC)
         _, _, _, g = O.combined_loss(res.acc, tg)
         np.testing.assert_allclose(g_dev[m].cpu().numpy(), O.contract(res.jac, g), rtol=RTOL_GRAD)
+
+
+def _flat(h, w):
+    z = np.zeros((h, w))
+    return F.Landscape(wind_speed=z.copy(), wind_direction=z.copy(), slope=np.zeros((h, w, 3, 3)),
+                       canopy=z.copy(), density=z.copy())
+
+
+def test_edge_cases_mirror_reference_kernel_tests():
+    """The reference's step semantics edge cases (pyrocell tests/test_kernel.py:220-284)."""
+    # no burning cells: fixed point, t advances
+    land = _flat(5, 5)
+    st = F.new_fire_state(np.zeros((5, 5), bool), land)
+    F.step_forward(st, land, F.ModelParams(), seed=9)
+    assert st.t == 1 and not st.burning.any() and not st.burned.any() and not st.accumulator.any()
+    # p_continue = 0 burns out in one step
+    init = np.zeros((5, 5), bool)
+    init[2, 2] = True
+    st = F.new_fire_state(init, land)
+    F.step_forward(st, land, F.ModelParams(p_h=0.2, p_continue=0.0), seed=1)
+    assert st.burned[2, 2] and not st.burning[2, 2]
+    # saturated spread grows one Moore ring per step
+    land = _flat(9, 9)
+    land.canopy[:] = 3.0
+    land.density[:] = 3.0
+    init = np.zeros((9, 9), bool)
+    init[4, 4] = True
+    st = F.new_fire_state(init, land)
+    for step in range(1, 4):
+        F.step_forward(st, land, F.ModelParams(p_h=1.0, p_continue=1.0), seed=5)
+        want = np.zeros((9, 9), bool)
+        want[4 - step:5 + step, 4 - step:5 + step] = True
+        assert np.array_equal(st.burning | st.burned, want)
+    # degenerate grids
+    sim = F.run_simulation(_flat(1, 8), F.ModelParams(p_h=0.9, p_continue=1.0),
+                           np.eye(1, 8, 3, dtype=bool), 5, seed=2)
+    assert sim.state.affected().sum() > 1
+    sim = F.run_simulation(_flat(1, 1), F.ModelParams(p_continue=0.0), np.ones((1, 1), bool), 3,
+                           seed=2)
+    assert sim.state.burned[0, 0] and not sim.state.burning[0, 0]
+    # zero steps returns the initial state; errors mirror the reference
+    sim = F.run_simulation(_flat(6, 6), F.ModelParams(), np.eye(6, dtype=bool), 0, seed=1)
+    assert sim.series == [] and np.array_equal(sim.state.burning, np.eye(6, dtype=bool))
+    with pytest.raises(ValueError, match="schedule step"):
+        F.run_simulation(_flat(4, 4), F.ModelParams(), np.zeros((4, 4), bool), 5, seed=0,
+                         wind_schedule=[F.WindUpdate(7, np.zeros((4, 4)), np.zeros((4, 4)))])
+    with pytest.raises(ValueError, match="steps must be"):
+        F.run_simulation(_flat(4, 4), F.ModelParams(), np.zeros((4, 4), bool), -1, seed=0)
+    with pytest.raises(ValueError, match="factor_site"):
+        F.run_simulation(_flat(4, 4), F.ModelParams(), np.zeros((4, 4), bool), 1, seed=0,
+                         factor_site="nowhere")
+
+
+def test_invariants_at_config1_size():
+    """Size-independent properties at BASELINE config-1 size (2048^2, 4 of
+    the 16 members, 500 steps): exclusivity, burned monotone via counters,
+    accumulator support == affected set, p in (0, 1], and one member
+    against the CPU oracle (bit-exact states)."""
+    n, steps, M = 2048, 500, 4
+    env = S.make_environment(n, seed=1)
+    dl = F.DeviceLandscape.from_environment(env)
+    ph = S.ensemble_ph(16)
+    b = F.FireBatch((n, n), M, max_steps=steps)
+    b.set_params(np.array([F.pack_params(0.045, 0.131, 0.078, ph[m], 0.3) for m in range(M)]))
+    b.set_seeds(list(range(M)))
+    init = S.center_ignition(n)
+    b.reset(init)
+    b.run(dl, steps)
+    bu, bd = b.unpack()
+    assert not (bu & bd).any()
+    aff = (bu | bd).bool()
+    acc = b.acc
+    assert torch.equal(acc > 0, aff)
+    assert float(acc.max()) <= 1.0
+    ser = b.series()
+    assert np.all(np.diff(ser[:, :, 1], axis=1) >= 0)
+    assert np.array_equal(ser[:, -1].sum(-1), aff.reshape(M, -1).sum(-1).cpu().numpy())
+    arr = S.reference_landscape_arrays(env, O.slope_from_altitude)
+    res = O.run(**arr, params=P([0.045, 0.131, 0.078, ph[2], 0.3]), init=init, steps=steps,
+                seed=2, threads=8, want_jac=False)
+    assert np.array_equal(bu[2].bool().cpu().numpy(), res.burning)
+    assert np.array_equal(bd[2].bool().cpu().numpy(), res.burned)
+    np.testing.assert_allclose(acc[2].double().cpu().numpy(), res.acc, rtol=RTOL_ACC)
