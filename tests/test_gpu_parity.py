@@ -445,3 +445,51 @@ def test_invariants_at_config1_size():
     assert np.array_equal(bu[2].bool().cpu().numpy(), res.burning)
     assert np.array_equal(bd[2].bool().cpu().numpy(), res.burned)
     np.testing.assert_allclose(acc[2].double().cpu().numpy(), res.acc, rtol=RTOL_ACC)
+
+
+def _small_calibration_problem():
+    size = 32
+    env = S.make_environment(size, seed=5)
+    arr = S.reference_landscape_arrays(env, O.slope_from_altitude)
+    d = load("calibrate_small")
+    land = F.Landscape(**arr)
+    sched = F.ObservationSchedule([F.Observation(target=t) for t in d["targets"]], 6)
+    start = F.ModelParams(c1=0.0, c2=0.0, a=0.0, p_h=0.3, p_continue=0.5)
+    return land, S.center_ignition(size), sched, start
+
+
+def test_device_and_host_calibration_drivers_agree():
+    land, init, sched, start = _small_calibration_problem()
+    a = F.calibrate(land, init, sched, start, F.StepRings(1, 2, 3), max_epochs=3, base_seed=5,
+                    learning_rate=0.05, device_driver=True)
+    b = F.calibrate(land, init, sched, start, F.StepRings(1, 2, 3), max_epochs=3, base_seed=5,
+                    learning_rate=0.05, device_driver=False)
+    ra = np.array([[r.loss, r.bce, r.mse, r.jaccard, r.manhattan] for r in a.records])
+    rb = np.array([[r.loss, r.bce, r.mse, r.jaccard, r.manhattan] for r in b.records])
+    np.testing.assert_allclose(ra, rb, rtol=1e-12)
+    ta = np.array([p.as_array() for _, _, p in a.manifest.trajectory])
+    tb = np.array([p.as_array() for _, _, p in b.manifest.trajectory])
+    np.testing.assert_allclose(ta, tb, rtol=1e-12, atol=1e-15)
+    assert a.best_params.as_array() == pytest.approx(b.best_params.as_array(), rel=1e-12)
+
+
+def test_calibration_aborts_epoch_on_non_finite_gradient(monkeypatch):
+    """calibration.py:217-221 (fault injection as in tests/test_calibrate.py:165-187)."""
+    land, init, sched, start = _small_calibration_problem()
+    orig = F.FireBatch.loss_grad
+    calls = {"n": 0}
+
+    def faulty(self, *a, **kw):
+        out = orig(self, *a, **kw)
+        calls["n"] += 1
+        if calls["n"] == 2:  # second iteration of the first epoch
+            out[2].fill_(float("nan"))
+        return out
+
+    monkeypatch.setattr(F.FireBatch, "loss_grad", faulty)
+    res = F.calibrate(land, init, sched, start, F.StepRings(1, 2, 3), max_epochs=2, base_seed=5,
+                      learning_rate=0.05)
+    assert res.aborted_epochs and res.aborted_epochs[0][0] == 1
+    assert "non-finite gradient" in res.aborted_epochs[0][1]
+    epochs = [r.epoch for r in res.records]
+    assert epochs.count(2) == 3  # the next epoch runs in full
