@@ -444,36 +444,21 @@ def bench_ensemble_calibration(dev, rank, world, members_total=256, iters=3):
     targets = torch.stack(targets)
     del tb
     mine = shard_members(members_total, rank, world)
-    b = F.FireBatch((n, n), len(mine), max_steps=T, with_jacobian=True, device=dev)
+    from paper_2502_18738_b200.ensemble import EnsembleCalibrator
     p0 = S.DEFAULT_BENCH_PARAMS
-    b.set_params(F.pack_params(p0["c1"], p0["c2"], p0["a"], p0["p_h"], p0["p_continue"]))
-    b.set_seeds(mine)
-    attach = [True] * T
-    shared = torch.zeros((1, 8), dtype=torch.float64, device=dev)
-    shared.copy_(b.params[:1])
-    adam = torch.zeros((1, 8), dtype=torch.float64, device=dev)
-    from paper_2502_18738_b200 import _lib as L
-
-    def iteration(k):
-        b.params.copy_(shared.expand_as(b.params))
-        b.reset(init)
-        b.run(dl, T, attach=attach, wind_schedule=sched)
-        loss, _, grad, _ = b.loss_grad(targets, obs)
-        g = grad.sum(0, keepdim=True)
-        allreduce_sum_(g)
-        L.check(L.lib().fc_adamw(g.data_ptr(), shared.data_ptr(), adam.data_ptr(), 1, k, None,
-                                 1e-2, 0.0, 0.9, 0.999, 1e-8, 1, None, L.stream_ptr()), "fc_adamw")
-        return loss
-
-    iteration(1)
+    cal = EnsembleCalibrator(dl, init, targets, obs, mine,
+                             (p0["c1"], p0["c2"], p0["a"], p0["p_h"], p0["p_continue"]),
+                             steps=T, wind_schedule=sched, lr=1e-2, device=dev)
+    cal.step()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    for k in range(2, 2 + iters):
-        loss = iteration(k)
+    for _ in range(iters):
+        loss = cal.step()
     e1.record()
     torch.cuda.synchronize()
     ms = allreduce_max(e0.elapsed_time(e1) / iters, dev)
+    shared = cal.shared
     return {"iter_per_s": 1e3 / ms, "ms_per_iter": ms, "members": members_total,
             "members_per_rank": len(mine), "grid": [n, n], "steps": T, "attached": "all",
             "fwd_bwd_cell_updates_per_s": members_total * n * n * T / (ms / 1e3),

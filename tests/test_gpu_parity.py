@@ -493,3 +493,36 @@ def test_calibration_aborts_epoch_on_non_finite_gradient(monkeypatch):
     assert "non-finite gradient" in res.aborted_epochs[0][1]
     epochs = [r.epoch for r in res.records]
     assert epochs.count(2) == 3  # the next epoch runs in full
+
+
+def test_ensemble_calibrator_gradient_sum_and_adam():
+    """Config-4 iteration on a small case: summed member gradients equal the
+    sum of the oracle's per-member gradients, and the shared parameters get
+    the reference AdamW + clamp step (calibration.py:43-64)."""
+    from paper_2502_18738_b200.device import scheduled_wind_fields, wind_ramp_schedule
+    from paper_2502_18738_b200.ensemble import EnsembleCalibrator
+    h, w, steps = 64, 72, 30
+    env = S.make_environment(h, w, seed=8)
+    dl = F.DeviceLandscape.from_environment(env)
+    sched = wind_ramp_schedule(steps, 2.0, 12.0, 90.0)
+    init = S.center_ignition(h, w)
+    targets = np.zeros((2, h, w), bool)
+    targets[0, 26:38, 30:42] = True
+    targets[1, 20:44, 24:50] = True
+    obs = [15, 30]
+    p0 = (0.045, 0.131, 0.078, 0.58, 0.3)
+    cal = EnsembleCalibrator(dl, init, torch.as_tensor(targets), obs, [0, 1, 2], p0, steps=steps,
+                             wind_schedule=sched, lr=1e-2)
+    cal.step()
+    arr = S.reference_landscape_arrays(env, O.slope_from_altitude)
+    rows = sched.cpu().numpy()
+    updates = [(t + 1, *scheduled_wind_fields(arr["wind_speed"], arr["wind_direction"], rows[t]))
+               for t in range(steps)]
+    total = np.zeros(4)
+    for m in range(3):
+        res = O.run(**arr, params=P(p0), init=init, steps=steps, seed=m,
+                    attach_steps=range(1, steps + 1), wind_schedule=updates)
+        total += O.multi_target_grad(res, obs, targets)[1]
+    st = {}
+    want = np.clip(O.adamw_update(st, np.array(p0[:4]), total, 1e-2), [0, 0, 0, 0.2], 1.0)
+    np.testing.assert_allclose(cal.params[:4], want, rtol=1e-9)
