@@ -25,9 +25,10 @@
  *                 the step a cell ignited in; -1 initial/injected; 0x7FFF
  *                 never); jacobian fp32 [M][H][W][4] = dp/d(c1,c2,a,p_h)
  *                 captured at ignition on attached steps (0 elsewhere).
- *   landscape     env fp32 [H][W][4] = {elevation m, wind vector east and
+ *   landscape     env fp32 [H][W][4] = {wind speed m/s, wind vector east and
  *                 north m/s (speed * cos/sin of the direction, deg East-CCW),
- *                 vd=(1+canopy)(1+density)};
+ *                 vd=(1+canopy)(1+density)}; slope4 fp32 [H][W][4] forward
+ *                 slopes from elevation (the fused slope_from_altitude);
  *                 env64 fp64 [H][W][5] = {elevation, speed, direction, canopy,
  *                 density} read only by the fp64 guard recompute; optional
  *                 slope tensors [H][W][8] (slot order NW,N,NE,W,E,SW,S,SE:
@@ -75,7 +76,11 @@ typedef struct {
 } fc_grid;
 
 typedef struct {
-    const float* env;       /* [H][W][4] fp32 {E, wind east, north, vd}  */
+    const float* env;       /* [H][W][4] fp32 {V, wind east, north, vd}  */
+    const float* slope4;    /* [H][W][4] fp32 slope in degrees (signed, slope_sign applied)
+                               from each cell toward its E, SW, S, SE neighbour (0 off-grid);
+                               the other four directions are the neighbours' negations
+                               (exact antisymmetry, data_io.py:112-129).  Elevation mode. */
     const double* env64;    /* [H][W][5] fp64                           */
     const float* slope32;   /* [H][W][8] fp32, FC_SLOPE_TENSOR only     */
     const double* slope64;  /* [H][W][8] fp64, FC_SLOPE_TENSOR only     */

@@ -41,7 +41,8 @@ class FcGrid(C.Structure):
 
 
 class FcLandscape(C.Structure):
-    _fields_ = [("env", C.c_void_p), ("env64", C.c_void_p), ("slope32", C.c_void_p),
+    _fields_ = [("env", C.c_void_p), ("slope4", C.c_void_p), ("env64", C.c_void_p),
+                ("slope32", C.c_void_p),
                 ("slope64", C.c_void_p), ("dir32", C.c_void_p), ("cell_side", C.c_double),
                 ("slope_mode", C.c_int32),
                 ("slope_sign", C.c_int32), ("factor_source", C.c_int32), ("pad_", C.c_int32)]

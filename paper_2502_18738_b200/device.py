@@ -36,12 +36,34 @@ def _dev(device) -> torch.device:
 
 
 def _fast_env(elev, speed, direction, canopy, density) -> torch.Tensor:
-    """fp32 [H][W][4] fast-path record: elevation, wind vector (east, north)
-    = speed * (cos, sin)(direction), and vd = (1 + canopy)(1 + density)."""
+    """fp32 [H][W][4] fast-path record: wind speed, wind vector (east,
+    north) = speed * (cos, sin)(direction), and vd = (1 + canopy)(1 + density)."""
     rad = direction * (np.pi / 180.0)
     vd = (1.0 + canopy) * (1.0 + density)
-    return torch.stack([elev, speed * torch.cos(rad), speed * torch.sin(rad), vd],
+    return torch.stack([speed, speed * torch.cos(rad), speed * torch.sin(rad), vd],
                        dim=-1).to(torch.float32).contiguous()
+
+
+def forward_slopes(elev: torch.Tensor, cell_side: float, sign: int = 1) -> torch.Tensor:
+    """fp32 [H][W][4] slope in degrees from each cell toward its E, SW, S, SE
+    neighbour, computed in fp64 like slope_from_altitude (data_io.py:92-132):
+    degrees(atan((E_i - E_j) / (k l))), k = sqrt(2) on diagonals, 0 where the
+    neighbour is off the grid; the opposite directions are exact negations."""
+    e = elev.to(torch.float64)
+    h, w = e.shape
+    out = torch.zeros((h, w, 4), dtype=torch.float64, device=e.device)
+    for j, (dr, dc) in enumerate(((0, 1), (1, -1), (1, 0), (1, 1))):
+        k = math.sqrt(2.0) if dr and dc else 1.0
+        r0, r1 = 0, h - dr
+        c0, c1 = max(-dc, 0), w - max(dc, 0)
+        if r1 <= r0 or c1 <= c0:
+            continue
+        src = e[r0:r1, c0:c1]
+        dst = e[r0 + dr:r1 + dr, c0 + dc:c1 + dc]
+        out[r0:r1, c0:c1, j] = torch.rad2deg(torch.atan((src - dst) / (k * cell_side)))
+    if sign < 0:
+        out = -out
+    return out.to(torch.float32).contiguous()
 
 
 class DeviceLandscape:
@@ -55,10 +77,13 @@ class DeviceLandscape:
 
     def __init__(self, env: torch.Tensor, env64: torch.Tensor, *, cell_side: float = 30.0,
                  slope32: Optional[torch.Tensor] = None, slope64: Optional[torch.Tensor] = None,
-                 slope_sign: int = 1, factor_site: str = "target"):
+                 slope_sign: int = 1, factor_site: str = "target",
+                 slope4: Optional[torch.Tensor] = None):
         if factor_site not in ("target", "source"):
             raise ValueError(f"factor_site must be 'target' or 'source', got {factor_site!r}")
         self.env, self.env64 = env.contiguous(), env64.contiguous()
+        self.slope4 = slope4 if slope4 is not None else forward_slopes(
+            self.env64[..., 0], cell_side, -1 if slope_sign < 0 else 1)
         rad = self.env64[..., 2] * (np.pi / 180.0)
         self.dir32 = torch.stack([torch.cos(rad), torch.sin(rad)], dim=-1).to(torch.float32).contiguous()
         self.slope32 = None if slope32 is None else slope32.contiguous()
@@ -126,12 +151,13 @@ class DeviceLandscape:
         env = _fast_env(env64[..., 0], v, d, env64[..., 3], env64[..., 4])
         out = DeviceLandscape(env, env64, cell_side=self.cell_side, slope32=self.slope32,
                               slope64=self.slope64, slope_sign=self.slope_sign,
-                              factor_site=self.factor_site)
+                              factor_site=self.factor_site, slope4=self.slope4)
         return out
 
     def struct(self) -> L.FcLandscape:
         s = L.FcLandscape()
         s.env, s.env64 = L.ptr(self.env), L.ptr(self.env64)
+        s.slope4 = L.ptr(self.slope4)
         s.slope32, s.slope64 = L.ptr(self.slope32), L.ptr(self.slope64)
         s.dir32 = L.ptr(self.dir32)
         s.cell_side = self.cell_side
@@ -143,7 +169,8 @@ class DeviceLandscape:
     @property
     def nbytes(self) -> int:
         return sum(t.numel() * t.element_size() for t in
-                   (self.env, self.env64, self.slope32, self.slope64) if t is not None)
+                   (self.env, self.slope4, self.env64, self.dir32, self.slope32, self.slope64)
+                   if t is not None)
 
 
 def wind_ramp_schedule(steps: int, v_start: float = 2.0, v_end: float = 12.0,
