@@ -45,8 +45,10 @@ def main():
               f"items mean {item[v, s_].mean():8.0f} max {item[v, s_].max():8.0f} cyc | "
               f"pool mean {tr[v, s_, 3].mean():6.0f} max {tr[v, s_, 3].max():6.0f}")
     print("tail (update) mean", nxt[valid[:, 1:]].mean() if valid[:, 1:].any() else None)
-    span = tr[:, :, 2].max(1) - tr[:, 0, 0]
-    print("per-CTA span mean", span.mean(), "max", span.max())
+    ok = (tr[:, :, 0] != 0).all(1) & (tr[:, :, 2] != 0).all(1)
+    span = tr[ok][:, :, 2].max(1) - tr[ok][:, 0, 0]
+    print("per-CTA span (first group) mean", span.mean(), "max", span.max(), "p90", np.percentile(span, 90))
+    print("step-time per CTA (bit+items+tail) mean", (tr[ok][:, 1:, 0] - tr[ok][:, :-1, 0]).mean())
 
 
 if __name__ == "__main__":
