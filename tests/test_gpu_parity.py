@@ -526,3 +526,30 @@ def test_ensemble_calibrator_gradient_sum_and_adam():
     st = {}
     want = np.clip(O.adamw_update(st, np.array(p0[:4]), total, 1e-2), [0, 0, 0, 0.2], 1.0)
     np.testing.assert_allclose(cal.params[:4], want, rtol=1e-9)
+
+
+@pytest.mark.parametrize("factor_site,slope_sign", [("source", "downhill-positive"),
+                                                     ("target", "uphill-positive")])
+def test_elevation_mode_options_match_oracle(factor_site, slope_sign):
+    """Native elevation mode with factor_site / slope_sign switches
+    (kernel.py:155-163, data_io.py:115-131) against the oracle."""
+    h, w, steps = 120, 90, 60
+    env = S.make_environment(h, w, seed=17)
+    dl = F.DeviceLandscape.from_environment(env, factor_site=factor_site, slope_sign=slope_sign)
+    init = S.center_ignition(h, w)
+    b = F.FireBatch((h, w), 1, max_steps=steps, with_jacobian=True)
+    b.set_params(F.pack_params(0.05, 0.12, 0.09, 0.55, 0.5))
+    b.set_seeds([9])
+    b.reset(init)
+    b.run(dl, steps, attach=[True] * steps)
+    arr = S.reference_landscape_arrays(env, lambda e, l: O.slope_from_altitude(e, l, slope_sign))
+    res = O.run(**arr, params=P([0.05, 0.12, 0.09, 0.55, 0.5]), init=init, steps=steps, seed=9,
+                attach_steps=range(1, steps + 1), factor_site=factor_site)
+    bu, bd = (x[0].bool().cpu().numpy() for x in b.unpack())
+    assert np.array_equal(bu, res.burning) and np.array_equal(bd, res.burned)
+    np.testing.assert_allclose(b.acc[0].double().cpu().numpy(), res.acc, rtol=RTOL_ACC)
+    tg = np.zeros((h, w), bool)
+    tg[40:80, 30:60] = True
+    _, _, g_dev, _ = b.loss_grad(torch.as_tensor(tg), [steps])
+    _, _, _, g = O.combined_loss(res.acc, tg)
+    np.testing.assert_allclose(g_dev[0].cpu().numpy(), O.contract(res.jac, g), rtol=RTOL_GRAD)
