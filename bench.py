@@ -188,7 +188,7 @@ def timed_loop(fn, K, flush):
     return [a.elapsed_time(b) for a, b in times]
 
 
-def launch_bytes(cnt, burning_pre, window, tiles_override=None):
+def launch_bytes(cnt, burning_pre, window, tiles_override=None, per_tile=512.0):
     """Algorithmic bytes of each window launch from the per-step counters:
     512 B per visited 32x32 tile (burning + burned words read and written
     once per launch), 16 B of env per ignition candidate and per burning
@@ -198,7 +198,7 @@ def launch_bytes(cnt, burning_pre, window, tiles_override=None):
     for a in range(0, steps, window):
         b = min(a + window, steps)
         tiles = cnt[a, 2] if tiles_override is None else tiles_override
-        out.append(512.0 * tiles + 16.0 * (cnt[a:b, 3].sum() + burning_pre[a:b].sum())
+        out.append(per_tile * tiles + 16.0 * (cnt[a:b, 3].sum() + burning_pre[a:b].sum())
                    + 6.0 * cnt[a:b, 0].sum())
     return np.array(out)
 
@@ -222,7 +222,7 @@ def per_launch_profile(batch, land, steps, window, skip=True):
     ser = batch.series()  # (M, steps, 2)
     burning_pre = np.concatenate([[batch.init_burning.sum()], ser[:, :-1, 0].sum(0)])[:steps]
     tiles = None if skip else batch.m * batch.grid.tiles_y * batch.grid.tiles_x
-    return ms, launch_bytes(cnt, burning_pre, window, tiles), cnt
+    return ms, launch_bytes(cnt, burning_pre, window, tiles, 512.0 if skip else 256.0), cnt
 
 
 def run_ours(args):
@@ -576,10 +576,37 @@ def bench_dense(dev, peak):
                     "achieved_GBps": ach, "frac_of_peak": ach / peak,
                     "bytes_per_launch": float(byts.mean()),
                     "tiles_per_launch": float(n * n / 1024 if not skip else cnt[::WINDOW, 2].mean())}
+        if not skip:
+            # the HBM-streaming half of the dense sweep on its own: the
+            # activity scan of the final state (reads the burning plane,
+            # writes one flag per tile and the zero next state of quiet tiles)
+            import ctypes as C
+            from paper_2502_18738_b200 import _lib as L
+            st = b.struct()
+            evs = []
+            for _ in range(20):
+                b.list_count.zero_()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                L.check(L.lib().fc_activity_scan(C.byref(b.grid), C.byref(st), b.q, L.stream_ptr()),
+                        "fc_activity_scan")
+                e1.record()
+                evs.append((e0, e1))
+            torch.cuda.synchronize()
+            sms = np.array([a.elapsed_time(c) for a, c in evs[2:]])
+            tiles = n * n // 1024
+            live = int(b.list_count[b.q].item())
+            sbytes = 128.0 * tiles + tiles + 128.0 * (tiles - live)  # plane read, flags, zero writes
+            ach_s = sbytes / (sms.mean() / 1e3) / 1e9
+            out["dense"]["activity_scan"] = {"avg_us": float(1e3 * sms.mean()),
+                                             "bytes": sbytes, "achieved_GBps": ach_s,
+                                             "frac_of_peak": ach_s / peak, "live_tiles": live}
         del b
-    out["note"] = ("dense = every 32x32 tile visited each launch (512 B per tile per launch of "
-                   "bit-plane traffic = 0.5/K B per cell-update); the SURVEY's 18 B/cell-update "
-                   "fp32-field design would cap the same sweep at peak/18 = 3.6e11 cu/s")
+    out["note"] = ("dense = every launch rescans the whole domain (fc_activity_scan: the burning "
+                   "plane read once, quiet tiles' next state written as zeros = 256 B per 32x32 "
+                   "tile per launch = 0.25/K B per cell-update) and advances the live tiles; "
+                   "skip = incremental activity lists.  The SURVEY's 18 B/cell-update fp32-field "
+                   "design would cap a dense sweep at peak/18 = 3.6e11 cu/s")
     return out
 
 

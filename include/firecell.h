@@ -105,6 +105,7 @@ typedef struct {
     int32_t* tile_list;     /* [3][M*TY*TX] rotating active-tile lists  */
     int32_t* list_count;    /* [2][max_steps+3]: list length, then work-
                                distribution counter, of each launch     */
+    uint8_t* tile_fire;     /* [M*TY*TX] scratch of the dense sweep     */
     int32_t max_steps;
     int32_t pad_;
 } fc_state;
@@ -151,7 +152,10 @@ int fc_inject(const fc_grid* g, const fc_state* s, const int32_t* cells, int32_t
  * host_attach: NULL or nsteps flags (step t0+i attaches when host_attach[i]).
  * draws: FC_RNG_INJECT only, [nsteps][M][2][H][W] fp64.
  * skip_inactive: 1 = only tiles near burning cells are visited (exact: the
- * analogue of the reference's bounding-box window, kernel.py:296-302).
+ * analogue of the reference's bounding-box window, kernel.py:296-302);
+ * 0 = dense sweep: every launch rescans the whole domain (fc_activity_scan)
+ * instead of using incremental activity lists.  A state must not switch
+ * between the two without fc_state_init.
  * window: steps fused per launch (temporal blocking; 1, 4, 8 or 16).
  * wind_schedule: NULL, or fp64 [max_steps][4] = {alpha, beta, gamma_deg, 0}
  * indexed by pre-step index: step t sees speed alpha*V + beta and direction
@@ -164,6 +168,12 @@ int fc_run(const fc_grid* g, const fc_landscape* land, const fc_state* s,
            const double* draws, int32_t t0, int32_t nsteps, const uint8_t* host_attach,
            int32_t skip_inactive, int32_t window, const double* wind_schedule,
            const fc_shard* shard, int32_t* host_phase, fc_stream_t stream);
+
+/* Dense-sweep activity scan for launch `phase` (the first half of every
+ * skip_inactive = 0 launch, exposed for measurement): streams the burning
+ * plane, lists every tile with fire in its 3x3 tile neighbourhood and writes
+ * the all-zero next state of every other tile (HBM-bound). */
+int fc_activity_scan(const fc_grid* g, const fc_state* s, int32_t phase, fc_stream_t stream);
 
 /* After the ghost rows were refreshed with the neighbours' state at launch
  * phase `phase`, activate the owned tiles next to ghost tiles holding fire

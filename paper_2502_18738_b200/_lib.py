@@ -30,7 +30,8 @@ NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", 
 
 # Every symbol include/firecell.h declares (checked by the CPU test suite).
 EXPORTS = ("fc_grid_make", "fc_plane_words", "fc_loss_workspace_bytes", "fc_state_init",
-           "fc_state_unpack", "fc_inject", "fc_run", "fc_mark_ghosts", "fc_contract", "fc_loss_grad",
+           "fc_state_unpack", "fc_inject", "fc_run", "fc_mark_ghosts", "fc_activity_scan",
+           "fc_contract", "fc_loss_grad",
            "fc_loss_dense", "fc_adamw", "fc_uniform_grid", "fc_epoch_seed", "fc_build_fields",
            "fc_last_cuda_error", "fc_version", "fc_debug_set_trace")
 
@@ -57,7 +58,7 @@ class FcState(C.Structure):
     _fields_ = [("burn0", C.c_void_p), ("burn1", C.c_void_p), ("burned", C.c_void_p),
                 ("acc", C.c_void_p), ("t_ign", C.c_void_p), ("jac", C.c_void_p),
                 ("flags", C.c_void_p), ("counters", C.c_void_p), ("tile_list", C.c_void_p),
-                ("list_count", C.c_void_p), ("max_steps", C.c_int32),
+                ("list_count", C.c_void_p), ("tile_fire", C.c_void_p), ("max_steps", C.c_int32),
                 ("pad_", C.c_int32)]
 
 
@@ -102,6 +103,7 @@ def lib():
             "fc_run": (C.c_int, [G, LS, ST, vp, vp, i32, vp, i32, i32, vp, i32, i32, vp, SH,
                                  C.POINTER(i32), vp]),
             "fc_mark_ghosts": (C.c_int, [G, ST, SH, i32, vp]),
+            "fc_activity_scan": (C.c_int, [G, ST, i32, vp]),
             "fc_contract": (C.c_int, [G, ST, vp, i32, vp, vp, vp]),
             "fc_loss_grad": (C.c_int, [G, ST, vp, i64, vp, i32, vp, vp, vp, vp, vp, vp]),
             "fc_loss_dense": (C.c_int, [i32, i32, vp, vp, vp, vp, vp, vp, vp]),

@@ -234,6 +234,8 @@ class FireBatch:
         ntiles = self.m * self.grid.tiles_y * self.grid.tiles_x
         self.tile_list = torch.empty((3, ntiles), dtype=torch.int32, device=dev)
         self.list_count = torch.zeros((2 * (self.max_steps + 3),), dtype=torch.int32, device=dev)
+        self.tile_fire = torch.zeros((ntiles,), dtype=torch.uint8, device=dev)
+        self._mode = None  # sweep mode since reset (activity lists vs dense rescans)
         self.params = torch.zeros((self.m, L.NPARAM), dtype=torch.float64, device=dev)
         self.seeds = torch.zeros((self.m,), dtype=torch.int64, device=dev)
         self.adam = torch.zeros((self.m, 8), dtype=torch.float64, device=dev)
@@ -254,6 +256,7 @@ class FireBatch:
         s.acc, s.t_ign, s.jac = L.ptr(self.acc), L.ptr(self.t_ign), L.ptr(self.jac)
         s.flags, s.counters = L.ptr(self.flags), L.ptr(self.counters)
         s.tile_list, s.list_count = L.ptr(self.tile_list), L.ptr(self.list_count)
+        s.tile_fire = L.ptr(self.tile_fire)
         s.max_steps = self.max_steps
         return s
 
@@ -297,6 +300,7 @@ class FireBatch:
                                       stride, int(t0), L.stream_ptr(stream)), "fc_state_init")
         self.t = int(t0)
         self.q = 0
+        self._mode = None
 
     def run(self, land: DeviceLandscape, nsteps: int, *, attach: Optional[Sequence[bool]] = None,
             rng: str = "splitmix", draws: Optional[torch.Tensor] = None, skip_inactive: bool = True,
@@ -325,6 +329,9 @@ class FireBatch:
             draws = draws.to(self.device, torch.float64).contiguous()
         if window not in (1, 4, 8, 16):
             raise ValueError("window must be 1, 4, 8 or 16")
+        if self._mode is not None and self._mode != bool(skip_inactive):
+            raise ValueError("skip_inactive cannot change between runs without reset()")
+        self._mode = bool(skip_inactive)
         if wind_schedule is not None:
             if tuple(wind_schedule.shape) != (self.max_steps, 4) or wind_schedule.dtype != torch.float64:
                 raise ValueError("wind_schedule must be fp64 of shape (max_steps, 4)")
