@@ -245,8 +245,13 @@ class FireBatch:
         self.workspace = torch.empty((ws,), dtype=torch.uint8, device=dev)
         self.t = 0
         self.q = 0  # launches since reset (burning-buffer parity, activity lists)
-        self.init_burning = np.zeros(self.m, dtype=np.int64)
+        self._init_burning_dev = torch.zeros((self.m,), dtype=torch.int64, device=dev)
         self._hw = hw
+
+    @property
+    def init_burning(self) -> np.ndarray:
+        """Burning cells per member at the last reset (host copy on demand)."""
+        return self._init_burning_dev.cpu().numpy().copy()
 
     # ------------------------------------------------------------ plumbing
     def struct(self) -> L.FcState:
@@ -286,14 +291,15 @@ class FireBatch:
             if tuple(m8.shape) != (self.h, self.w):
                 raise ValueError(f"initial fire mask shape {tuple(m8.shape)} != landscape {(self.h, self.w)}")
             stride = 0
-            per = int(m8.sum().item()) if not torch.cuda.is_current_stream_capturing() else 0
-            self.init_burning[:] = per
         elif m8.dim() == 3 and tuple(m8.shape) == (self.m, self.h, self.w):
             stride = self._hw
-            if not torch.cuda.is_current_stream_capturing():
-                self.init_burning[:] = m8.reshape(self.m, -1).sum(1).cpu().numpy()
         else:
             raise ValueError(f"initial fire mask must be 2-D or (M,H,W), got {tuple(m8.shape)}")
+        # initial burning counts stay on the device (no host sync inside a
+        # timed or captured sequence); series() reads them when asked
+        if not torch.cuda.is_current_stream_capturing():
+            cnt = (m8 != 0).reshape(-1, self._hw).sum(1, dtype=torch.int64)
+            self._init_burning_dev = cnt.expand(self.m) if m8.dim() == 2 else cnt
         self._init_mask = m8.contiguous()
         st = self.struct()
         L.check(L.lib().fc_state_init(C.byref(self.grid), C.byref(st), L.ptr(self._init_mask),

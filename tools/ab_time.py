@@ -49,6 +49,21 @@ def main():
         b2.reset(init2)
         b2.run(dl2, 100, attach=[True] * 100, window=window)
     print("c2 fwd(all attached) ms/iter %.3f" % timeit(c2fwd, 20))
+    if os.environ.get("AB_C3"):
+        n3 = 16384
+        e = S.make_environment_torch(n3, n3, seed=3, device="cuda")
+        dl3 = F.DeviceLandscape.from_elevation(e["elevation"], e["wind_speed"], e["wind_direction"],
+                                               e["canopy"], e["density"])
+        del e
+        b3 = F.FireBatch((n3, n3), 1, max_steps=200)
+        b3.set_params(F.pack_params(0.045, 0.131, 0.078, 0.58, 0.3))
+        b3.set_seeds([3])
+        init3 = torch.as_tensor(S.random_blocks(n3, n3, 8, 5, seed=3).astype(np.uint8), device="cuda")
+        for skip in (True, False):
+            def c3():
+                b3.reset(init3)
+                b3.run(dl3, 200, window=window, skip_inactive=skip)
+            print("c3 %s 200 steps ms %.3f" % ("skip" if skip else "dense", timeit(c3, 3)))
 
 
 if __name__ == "__main__":

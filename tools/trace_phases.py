@@ -1,5 +1,8 @@
-"""Phase timing of the window kernel from an FC_TRACE build:
-FIRECELL_SO=<trace build> python tools/trace_phases.py [launch_index]"""
+"""Per-warp phase timing of the window kernel from an FC_TRACE build:
+FIRECELL_SO=<trace build> python tools/trace_phases.py [c1|c3] [launch_index] [warps]
+
+Per (CTA, step, warp): step start, item-phase start (after barrier 1),
+item-phase end (before barrier 2), item rounds of the warp."""
 import os
 import sys
 
@@ -12,43 +15,76 @@ from paper_2502_18738_b200 import _lib as L  # noqa: E402
 from paper_2502_18738_b200 import synthetic as S  # noqa: E402
 
 
+def setup(work):
+    if work.startswith("c1"):
+        env = S.make_environment(2048, seed=1)
+        dl = F.DeviceLandscape.from_environment(env)
+        M = int(work[3:]) if work.startswith("c1m") else 16  # c1m1: one member
+        b = F.FireBatch((2048, 2048), M, max_steps=504)
+        ph = S.ensemble_ph(M)
+        b.set_params(np.array([F.pack_params(0.045, 0.131, 0.078, p, 0.3) for p in ph]))
+        b.set_seeds(list(range(M)))
+        b.reset(S.center_ignition(2048))
+        return dl, b
+    n = 16384
+    e = S.make_environment_torch(n, n, seed=3, device="cuda")
+    dl = F.DeviceLandscape.from_elevation(e["elevation"], e["wind_speed"], e["wind_direction"],
+                                          e["canopy"], e["density"])
+    del e
+    b = F.FireBatch((n, n), 1, max_steps=504)
+    b.set_params(F.pack_params(0.045, 0.131, 0.078, 0.58, 0.3))
+    b.set_seeds([3])
+    b.reset(S.random_blocks(n, n, 8, 5, seed=3))
+    return dl, b
+
+
 def main():
-    target = int(sys.argv[1]) if len(sys.argv) > 1 else 55
-    env = S.make_environment(2048, seed=1)
-    dl = F.DeviceLandscape.from_environment(env)
-    b = F.FireBatch((2048, 2048), 16, max_steps=504)
-    ph = S.ensemble_ph(16)
-    b.set_params(np.array([F.pack_params(0.045, 0.131, 0.078, p, 0.3) for p in ph]))
-    b.set_seeds(list(range(16)))
-    b.reset(S.center_ignition(2048))
-    trace = torch.zeros((512, 16, 4), dtype=torch.int64, device="cuda")
-    for q in range(63):
+    work = sys.argv[1] if len(sys.argv) > 1 else "c1"
+    target = int(sys.argv[2]) if len(sys.argv) > 2 else 30
+    warps = int(sys.argv[3]) if len(sys.argv) > 3 else 8
+    dl, b = setup(work)
+    trace = torch.zeros((512, 16, warps, 8), dtype=torch.int64, device="cuda")
+    for q in range(target + 1):
         if q == target:
             L.lib().fc_debug_set_trace(trace.data_ptr())
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
         b.run(dl, 8, window=8)
         if q == target:
+            e1.record()
             L.lib().fc_debug_set_trace(None)
     torch.cuda.synchronize()
-    tr = trace.cpu().numpy()
-    act = tr[:, 0, 0] != 0
+    print(f"{work} launch {target}: {1e3 * e0.elapsed_time(e1):.1f} us")
+    tr = trace.cpu().numpy().astype(np.float64)
+    act = tr[:, 0, 0, 0] != 0
     tr = tr[act]
-    print("CTAs traced", act.sum())
-    bit = tr[:, :, 1] - tr[:, :, 0]
-    item = tr[:, :, 2] - tr[:, :, 1]
-    nxt = tr[:, 1:, 0] - tr[:, :-1, 2]
-    valid = (tr[:, :, 0] != 0) & (tr[:, :, 2] != 0)
+    print("CTAs traced", int(act.sum()))
+    first = tr[:, 0, :, 0]
+    first = first[first > 0]
+    last = tr[:, :, :, 2].max()
+    print(f"span first step start -> last item end: {last - first.min():.0f} cycles "
+          f"({(last - first.min()) / 1965:.1f} us at 1965 MHz)")
     for s_ in range(8):
-        v = valid[:, s_]
-        if not v.any():
+        st = tr[:, s_]  # (cta, warp, 4)
+        ok = (st[:, :, 1] != 0).all(1) & (st[:, :, 2] != 0).all(1)
+        if not ok.any():
             continue
-        print(f"step {s_}: bit phase mean {bit[v, s_].mean():8.0f} max {bit[v, s_].max():8.0f} cyc | "
-              f"items mean {item[v, s_].mean():8.0f} max {item[v, s_].max():8.0f} cyc | "
-              f"pool mean {tr[v, s_, 3].mean():6.0f} max {tr[v, s_, 3].max():6.0f}")
-    print("tail (update) mean", nxt[valid[:, 1:]].mean() if valid[:, 1:].any() else None)
-    ok = (tr[:, :, 0] != 0).all(1) & (tr[:, :, 2] != 0).all(1)
-    span = tr[ok][:, :, 2].max(1) - tr[ok][:, 0, 0]
-    print("per-CTA span (first group) mean", span.mean(), "max", span.max(), "p90", np.percentile(span, 90))
-    print("step-time per CTA (bit+items+tail) mean", (tr[ok][:, 1:, 0] - tr[ok][:, :-1, 0]).mean())
+        st = st[ok]
+        sweep = st[:, :, 1].min(1) - st[:, :, 0].min(1)        # step start -> barrier-1 release
+        items = st[:, :, 2].max(1) - st[:, :, 1].min(1)         # release -> last warp done
+        wdur = st[:, :, 2] - st[:, :, 1]
+        rounds = st[:, :, 3]
+        nxt = (tr[ok][:, s_ + 1, :, 0].min(1) - st[:, :, 2].max(1)) if s_ < 7 else np.zeros(1)
+        print(f"step {s_}: CTAs {ok.sum():4d} | start->release {sweep.mean():6.0f} | items crit "
+              f"{items.mean():6.0f} (p90 {np.percentile(items, 90):6.0f} max {items.max():6.0f}) | "
+              f"warp item dur mean {wdur.mean():6.0f} | rounds mean {rounds.mean():4.2f} max "
+              f"{rounds.max():.0f} | tail {nxt.mean():6.0f}")
+        it = st.reshape(-1, 8)
+        it = it[(it[:, 4] > 0) & (it[:, 7] > 0)]
+        if len(it):
+            print(f"        candidate item (lane 0): start->entry {np.median(it[:, 4] - it[:, 1]):6.0f} "
+                  f"live+draw {np.median(it[:, 5] - it[:, 4]):6.0f} slots {np.median(it[:, 6] - it[:, 5]):6.0f} "
+                  f"decide {np.median(it[:, 7] - it[:, 6]):6.0f} (medians over {len(it)} warps)")
 
 
 if __name__ == "__main__":
