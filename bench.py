@@ -46,7 +46,7 @@ CONFIG = {"workload": "c1_ensemble_forward", "members_per_gpu": MEMBERS, "grid":
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-extras", action="store_true", help="skip calibration/dense probes")
@@ -65,22 +65,41 @@ def load_peaks():
 
 # ------------------------------------------------------------------ clocks ---
 class ClockSampler:
-    """nvidia-smi -lms 200 during the timed region (B200_PROFILING.md)."""
+    """SM clocks and throttle reasons sampled DURING the timed region: NVML
+    every 5 ms on the box (the timed region is tens of ms), else nvidia-smi
+    -lms 100 (B200_PROFILING.md clocks line)."""
 
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    # NVML clocks-event-reason bits
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown"}
 
     def __init__(self, gpu_index: int):
         self.gpu = gpu_index
         self.proc = None
         self.lines = []
+        self.sm, self.mx, self.reasons = [], None, set()
+        self.nvml = None
+        self._stop = threading.Event()
 
     def __enter__(self):
         try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+            self.mx = float(pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM))
+            self.t = threading.Thread(target=self._poll, daemon=True)
+            self.t.start()
+            return self
+        except Exception:
+            self.nvml = None
+        try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "200", "-i", str(self.gpu)], stdout=subprocess.PIPE,
+                 "-lms", "100", "-i", str(self.gpu)], stdout=subprocess.PIPE,
                 stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -88,11 +107,28 @@ class ClockSampler:
             self.proc = None
         return self
 
+    def _poll(self):
+        p = self.nvml
+        while not self._stop.is_set():
+            try:
+                self.sm.append(float(p.nvmlDeviceGetClockInfo(self.h, p.NVML_CLOCK_SM)))
+                bits = p.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for b, n in self.REASONS.items():
+                    if bits & b:
+                        self.reasons.add(n)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
     def __exit__(self, *exc):
+        if self.nvml is not None:
+            self._stop.set()
+            self.t.join(timeout=1)
+            return
         if self.proc is not None:
             time.sleep(0.25)
             self.proc.terminate()
@@ -102,7 +138,7 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
+        sm, mx, reasons = list(self.sm), self.mx, set(self.reasons)
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
             parts = [p.strip() for p in ln.split(",")]
@@ -116,10 +152,11 @@ class ClockSampler:
             for n, v in zip(names, parts[5:9]):
                 if v.lower().startswith("active"):
                     reasons.add(n)
+        src = "nvml 5 ms" if self.nvml is not None else "nvidia-smi 100 ms"
         if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": [], "samples": 0}
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": [], "samples": 0, "source": src}
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "source": src}
 
 
 # ----------------------------------------------------------- reference arm ---
@@ -274,22 +311,35 @@ def run_ours(args):
     affected_final = int(ser[:, -1].sum())
 
     # -------------------------------------------------- roofline (live)
+    # achieved = SURVEY.md 8(d) algorithmic bytes per cell-update x the
+    # cell-updates the launches process / their CUDA-event time.  8(d):
+    # B(M, k) = (16/M + 2)/k B per cell-update (16 B of fp32 env shared by M
+    # members, 1 B state read + 1 B written, once per k fused steps).
     lms, lbytes, cnt = per_launch_profile(batch, dl, STEPS, WINDOW)
-    achieved = float(lbytes.sum() / (lms.sum() / 1e3)) / 1e9
+    b_cu = (16.0 / MEMBERS + 2.0) / WINDOW
+    run_cu = MEMBERS * H * W * STEPS
+    achieved = b_cu * run_cu / (lms.sum() / 1e3) / 1e9
+    kern = float(lbytes.sum() / (lms.sum() / 1e3)) / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
                 "kernel": f"window_kernel<SPLITMIX,elev,no-attach,K={WINDOW}>",
-                "avg_launch_us": float(1e3 * lms.mean()),
-                "algorithmic_bytes_per_launch": float(lbytes.mean()),
+                "avg_launch_us": float(1e3 * lms.mean()), "launches": int(len(lms)),
+                "algorithmic_bytes_per_cell_update": b_cu,
+                "algorithmic_bytes_per_launch": b_cu * run_cu / len(lms),
+                "kernel_bytes_per_launch": float(lbytes.mean()),
+                "kernel_bytes_GBps": kern, "kernel_bytes_frac": kern / peak,
                 "tiles_visited_per_launch": float(cnt[::WINDOW, 2].mean()),
-                "note": "activity-skipping sweep: only tiles near fire are visited, so the "
-                        "launch is latency-bound; see dense_probe for the full-domain sweep"}
+                "note": "achieved/frac: SURVEY 8(d) B(M=16,k=8)=0.375 B/cell-update over every "
+                        "cell of every member; the kernel itself touches only tiles near fire "
+                        "(kernel_bytes: 512 B per visited 32x32 tile + 16 B env per work item "
+                        "+ 6 B per ignition), so its own traffic is far below the 8(d) figure "
+                        "and it is latency-bound (DESIGN.md 3)"}
     prof = os.path.join(REPO, "profiles", "ncu_traffic.json")
     if os.path.exists(prof):
         with open(prof) as f:
             tr = json.load(f)
         roofline["traffic"] = tr.get("c1_step_kernel_dram_bytes_per_launch")
-
+        roofline["traffic_source"] = tr.get("source")
     # -------------------------------------------------------------- e2e
     runner = EnsembleRunner((H, W), MEMBERS, STEPS, device=dev)
     env_host = torch.stack([torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)) for a in
@@ -571,8 +621,12 @@ def bench_dense(dev, peak):
         ms, byts, cnt = per_launch_profile(b, dl, steps, WINDOW, skip)
         ach = float(byts.sum() / (ms.sum() / 1e3)) / 1e9
         key = "skip" if skip else "dense"
+        cups = n * n * steps / (ms.sum() / 1e3)
+        b_cu = (16.0 + 2.0) / WINDOW  # SURVEY 8(d) B(M=1, k)
         out[key] = {"avg_launch_us": float(1e3 * ms.mean()),
-                    "cell_updates_per_s": n * n * steps / (ms.sum() / 1e3),
+                    "cell_updates_per_s": cups,
+                    "survey_bytes_per_cell_update": b_cu,
+                    "survey_equiv_GBps": b_cu * cups / 1e9,
                     "achieved_GBps": ach, "frac_of_peak": ach / peak,
                     "bytes_per_launch": float(byts.mean()),
                     "tiles_per_launch": float(n * n / 1024 if not skip else cnt[::WINDOW, 2].mean())}
