@@ -234,6 +234,21 @@ uint64_t fc_epoch_seed(uint64_t base_seed, uint64_t epoch);
 int fc_build_fields(const fc_grid* g, const fc_landscape* land, const double* params,
                     double* out, int32_t with_gradients, fc_stream_t stream);
 
+/* ---------------------------------------------------------- landscape --- */
+/* Kernel-layout landscape from the five rasters (Landscape, model.py:76-105;
+ * slope_from_altitude, data_io.py:92-132) in one pass: inputs [H][W] fp32
+ * (input_is_f64 = 0) or fp64; outputs env fp32 [H][W][4] = {V, V cos th,
+ * V sin th, (1+canopy)(1+density)}, slope4 fp32 [H][W][4] = slope in degrees
+ * toward the E, SW, S, SE neighbour (0 off the grid; negated when
+ * slope_sign < 0), env64 fp64 [H][W][5] = the inputs widened, dir32 fp32
+ * [H][W][2] = (cos th, sin th).  All arithmetic in fp64 before rounding,
+ * like the reference (replaces the host-side torch preparation). */
+int fc_landscape_build(int32_t height, int32_t width, const void* elevation,
+                       const void* wind_speed, const void* wind_direction, const void* canopy,
+                       const void* density, int32_t input_is_f64, double cell_side,
+                       int32_t slope_sign, float* env, float* slope4, double* env64, float* dir32,
+                       fc_stream_t stream);
+
 /* ---------------------------------------------------------- diagnostics --- */
 int fc_last_cuda_error(void);
 const char* fc_version(void);

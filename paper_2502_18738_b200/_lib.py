@@ -33,6 +33,7 @@ EXPORTS = ("fc_grid_make", "fc_plane_words", "fc_loss_workspace_bytes", "fc_stat
            "fc_state_unpack", "fc_inject", "fc_run", "fc_mark_ghosts", "fc_activity_scan",
            "fc_contract", "fc_loss_grad",
            "fc_loss_dense", "fc_adamw", "fc_uniform_grid", "fc_epoch_seed", "fc_build_fields",
+           "fc_landscape_build",
            "fc_last_cuda_error", "fc_version", "fc_debug_set_trace")
 
 
@@ -111,6 +112,8 @@ def lib():
             "fc_uniform_grid": (C.c_int, [u64, i64, i32, i64, i64, i64, i64, vp, vp]),
             "fc_epoch_seed": (u64, [u64, u64]),
             "fc_build_fields": (C.c_int, [G, LS, vp, vp, i32, vp]),
+            "fc_landscape_build": (C.c_int, [i32, i32, vp, vp, vp, vp, vp, i32, dbl, i32, vp, vp,
+                                             vp, vp, vp]),
             "fc_last_cuda_error": (C.c_int, []),
             "fc_version": (C.c_char_p, []),
             "fc_debug_set_trace": (None, [vp]),

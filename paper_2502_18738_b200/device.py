@@ -78,14 +78,16 @@ class DeviceLandscape:
     def __init__(self, env: torch.Tensor, env64: torch.Tensor, *, cell_side: float = 30.0,
                  slope32: Optional[torch.Tensor] = None, slope64: Optional[torch.Tensor] = None,
                  slope_sign: int = 1, factor_site: str = "target",
-                 slope4: Optional[torch.Tensor] = None):
+                 slope4: Optional[torch.Tensor] = None, dir32: Optional[torch.Tensor] = None):
         if factor_site not in ("target", "source"):
             raise ValueError(f"factor_site must be 'target' or 'source', got {factor_site!r}")
         self.env, self.env64 = env.contiguous(), env64.contiguous()
         self.slope4 = slope4 if slope4 is not None else forward_slopes(
             self.env64[..., 0], cell_side, -1 if slope_sign < 0 else 1)
-        rad = self.env64[..., 2] * (np.pi / 180.0)
-        self.dir32 = torch.stack([torch.cos(rad), torch.sin(rad)], dim=-1).to(torch.float32).contiguous()
+        if dir32 is None:
+            rad = self.env64[..., 2] * (np.pi / 180.0)
+            dir32 = torch.stack([torch.cos(rad), torch.sin(rad)], dim=-1).to(torch.float32)
+        self.dir32 = dir32.contiguous()
         self.slope32 = None if slope32 is None else slope32.contiguous()
         self.slope64 = None if slope64 is None else slope64.contiguous()
         self.cell_side = float(cell_side)
@@ -105,13 +107,28 @@ class DeviceLandscape:
             raise ValueError(f"unknown slope_sign {slope_sign!r}")
         if cell_side <= 0:
             raise ValueError("cell_side must be > 0")
-        t64 = [torch.as_tensor(np.asarray(a) if not torch.is_tensor(a) else a).to(dev, torch.float64)
-               for a in (elevation, wind_speed, wind_direction, canopy, density)]
-        env64 = torch.stack(t64, dim=-1)
-        env = _fast_env(t64[0], t64[1], t64[2], t64[3], t64[4])
-        return cls(env, env64, cell_side=cell_side,
-                   slope_sign=-1 if slope_sign == "uphill-positive" else 1,
-                   factor_site=factor_site)
+        ts = [torch.as_tensor(np.asarray(a) if not torch.is_tensor(a) else a)
+              for a in (elevation, wind_speed, wind_direction, canopy, density)]
+        shape = tuple(ts[0].shape)
+        if len(shape) != 2 or any(tuple(t.shape) != shape for t in ts):
+            raise ValueError("landscape rasters must be 2-D and of one shape")
+        # fp32 rasters stay fp32 (widened exactly in the kernel); anything
+        # else is taken in fp64
+        dt = torch.float32 if all(t.dtype == torch.float32 for t in ts) else torch.float64
+        ts = [t.to(dev, dt).contiguous() for t in ts]
+        h, w = shape
+        env = torch.empty((h, w, 4), dtype=torch.float32, device=dev)
+        slope4 = torch.empty((h, w, 4), dtype=torch.float32, device=dev)
+        env64 = torch.empty((h, w, 5), dtype=torch.float64, device=dev)
+        dir32 = torch.empty((h, w, 2), dtype=torch.float32, device=dev)
+        sign = -1 if slope_sign == "uphill-positive" else 1
+        with torch.cuda.device(dev):
+            L.check(L.lib().fc_landscape_build(
+                h, w, *[L.ptr(t) for t in ts], 1 if dt == torch.float64 else 0, float(cell_side),
+                sign, L.ptr(env), L.ptr(slope4), L.ptr(env64), L.ptr(dir32), L.stream_ptr()),
+                "fc_landscape_build")
+        return cls(env, env64, cell_side=cell_side, slope_sign=sign, factor_site=factor_site,
+                   slope4=slope4, dir32=dir32)
 
     @classmethod
     def from_environment(cls, env, **kw) -> "DeviceLandscape":

@@ -43,6 +43,10 @@ class EnsembleRunner:
         self.out_d = _pinned((self.m, self.h, self.w), torch.uint8)
         self.out_acc = _pinned((self.m, self.h, self.w), torch.float32)
         self.out_cnt = _pinned((self.m, max(steps, 1), 4), torch.int32)
+        self.out_init = _pinned((self.m,), torch.int64)
+        self.in_params = _pinned((self.m, 8), torch.float64)
+        self.in_seeds = _pinned((self.m,), torch.int64)
+        self.copy_stream = torch.cuda.Stream(device=dev)
         self.h2d_bytes = self.env_dev.numel() * 4 + self.init_dev.numel()
         self.d2h_bytes = (self.out_b.numel() * 2 + self.out_acc.numel() * 4
                           + self.m * self.steps * 4 * 4)
@@ -53,27 +57,39 @@ class EnsembleRunner:
         """env_host: (5, H, W) fp32 (elevation, speed, direction, canopy,
         density), ideally pinned; init_host: (H, W) uint8/bool;
         params: per-member (c1, c2, a, p_h, p_continue)."""
+        from .device import _u64_to_i64
+        st = torch.cuda.current_stream(self.dev)
+        st.wait_stream(self.copy_stream)  # the previous call's accumulator copy is done
         self.env_dev.copy_(env_host, non_blocking=True)
         self.init_dev.copy_(init_host, non_blocking=True)
         e = self.env_dev
         land = DeviceLandscape.from_elevation(e[0], e[1], e[2], e[3], e[4],
                                               cell_side=self.cell_side, device=self.dev)
-        p8 = np.array([pack_params(*p, norm_c) for p in params], dtype=np.float64)
-        self.batch.set_params(p8.reshape(self.m, -1))
-        self.batch.set_seeds(list(seeds))
+        self.in_params.numpy()[:] = np.array([pack_params(*p, norm_c) for p in params],
+                                             dtype=np.float64).reshape(self.m, -1)
+        sd = [_u64_to_i64(v) for v in np.atleast_1d(np.asarray(seeds, dtype=object))]
+        self.in_seeds.numpy()[:] = sd * self.m if len(sd) == 1 else sd
+        self.batch.params.copy_(self.in_params, non_blocking=True)
+        self.batch.seeds.copy_(self.in_seeds, non_blocking=True)
         self.batch.reset(self.init_dev)
         self.batch.run(land, self.steps, rng=self.rng)
+        # the accumulator leaves on a side stream while the states unpack
+        done = torch.cuda.Event()
+        done.record(st)
+        with torch.cuda.stream(self.copy_stream):
+            self.copy_stream.wait_event(done)
+            self.out_acc.copy_(self.batch.acc, non_blocking=True)
         b, d = self.batch.unpack()
         self.out_b.copy_(b, non_blocking=True)
         self.out_d.copy_(d, non_blocking=True)
-        self.out_acc.copy_(self.batch.acc, non_blocking=True)
         self.out_cnt.copy_(self.batch.counters[:, : max(self.steps, 1)], non_blocking=True)
+        self.out_init.copy_(self.batch._init_burning_dev, non_blocking=True)
+        self.batch.acc.record_stream(self.copy_stream)
         if sync:
-            torch.cuda.current_stream().synchronize()
+            st.synchronize()
+            self.copy_stream.synchronize()
         cnt = self.out_cnt.numpy()[:, : self.steps].astype(np.int64)
-        init_n = int(np.asarray(init_host).sum()) if not torch.is_tensor(init_host) else \
-            int(init_host.sum())
-        burning = init_n + np.cumsum(cnt[:, :, 0] - cnt[:, :, 1], axis=1)
+        burning = self.out_init.numpy()[:, None] + np.cumsum(cnt[:, :, 0] - cnt[:, :, 1], axis=1)
         burned = np.cumsum(cnt[:, :, 1], axis=1)
         return EnsembleResult(self.out_b.numpy(), self.out_d.numpy(), self.out_acc.numpy(),
                               np.stack([burning, burned], axis=-1))

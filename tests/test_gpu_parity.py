@@ -553,3 +553,66 @@ def test_elevation_mode_options_match_oracle(factor_site, slope_sign):
     _, _, g_dev, _ = b.loss_grad(torch.as_tensor(tg), [steps])
     _, _, _, g = O.combined_loss(res.acc, tg)
     np.testing.assert_allclose(g_dev[0].cpu().numpy(), O.contract(res.jac, g), rtol=RTOL_GRAD)
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_landscape_build_kernel_matches_fp64_preparation(dtype):
+    """fc_landscape_build against the fp64 preparation it replaces (torch
+    ops in the reference's operation order; slope_from_altitude via the
+    oracle for the slope field): env64 exact, fp32 fields equal after one
+    rounding, off-grid slopes 0, both slope signs."""
+    from paper_2502_18738_b200.device import forward_slopes
+    rng = np.random.default_rng(5)
+    h, w = 37, 53
+    el = (rng.random((h, w)) * 1500).astype(dtype)
+    sp = (rng.random((h, w)) * 10).astype(dtype)
+    di = (rng.random((h, w)) * 360).astype(dtype)
+    ca = rng.choice([-0.3, 0.0, 0.4], (h, w)).astype(dtype)
+    de = rng.choice([-0.4, 0.0, 0.3], (h, w)).astype(dtype)
+    for sign in ("downhill-positive", "uphill-positive"):
+        dl = F.DeviceLandscape.from_elevation(el, sp, di, ca, de, cell_side=30.0, slope_sign=sign)
+        t64 = [torch.as_tensor(a.astype(np.float64), device="cuda") for a in (el, sp, di, ca, de)]
+        np.testing.assert_array_equal(dl.env64.cpu().numpy(),
+                                      np.stack([a.astype(np.float64) for a in (el, sp, di, ca, de)], -1))
+        rad = t64[2] * (np.pi / 180.0)
+        ref_env = torch.stack([t64[1], t64[1] * torch.cos(rad), t64[1] * torch.sin(rad),
+                               (1.0 + t64[3]) * (1.0 + t64[4])], -1).to(torch.float32)
+        np.testing.assert_array_equal(dl.env.cpu().numpy(), ref_env.cpu().numpy())
+        ref_dir = torch.stack([torch.cos(rad), torch.sin(rad)], -1).to(torch.float32)
+        np.testing.assert_array_equal(dl.dir32.cpu().numpy(), ref_dir.cpu().numpy())
+        ref_s4 = forward_slopes(t64[0], 30.0, -1 if sign == "uphill-positive" else 1)
+        np.testing.assert_array_equal(dl.slope4.cpu().numpy(), ref_s4.cpu().numpy())
+        # the oracle's slope_from_altitude (reference semantics) agrees in fp32
+        s33 = O.slope_from_altitude(el.astype(np.float64), 30.0, sign)
+        for j, (dr, dc) in enumerate(((0, 1), (1, -1), (1, 0), (1, 1))):
+            np.testing.assert_array_equal(dl.slope4.cpu().numpy()[..., j],
+                                          s33[:, :, 1 + dr, 1 + dc].astype(np.float32))
+
+
+def test_ensemble_runner_host_api_matches_device_batch():
+    """EnsembleRunner (host buffers in, host results out; the bench e2e
+    call) returns exactly what a FireBatch run on the same inputs holds."""
+    from paper_2502_18738_b200.ensemble import EnsembleRunner
+    n, m, steps = 160, 3, 60
+    env = S.make_environment(n, seed=4)
+    env_host = torch.stack([torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)) for a in
+                            (env.elevation, env.wind_speed, env.wind_direction, env.canopy,
+                             env.density)]).pin_memory()
+    init = S.center_ignition(n)
+    params = [(0.045, 0.131, 0.078, p, 0.3) for p in (0.5, 0.58, 0.66)]
+    seeds = [11, 12, 13]
+    r = EnsembleRunner((n, n), m, steps)
+    out = None
+    for _ in range(2):  # buffers are reused between calls
+        out = r(env_host, torch.from_numpy(init.astype(np.uint8)), params, seeds)
+    dl = F.DeviceLandscape.from_elevation(*[env_host[i].cuda() for i in range(5)])
+    b = F.FireBatch((n, n), m, max_steps=steps)
+    b.set_params(np.array([F.pack_params(*p) for p in params]))
+    b.set_seeds(seeds)
+    b.reset(init)
+    b.run(dl, steps)
+    bu, bd = b.unpack()
+    np.testing.assert_array_equal(out.burning, bu.cpu().numpy())
+    np.testing.assert_array_equal(out.burned, bd.cpu().numpy())
+    np.testing.assert_array_equal(out.accumulator, b.acc.cpu().numpy())
+    np.testing.assert_array_equal(out.series, b.series())
