@@ -106,6 +106,11 @@ typedef struct {
     int32_t* list_count;    /* [2][max_steps+3]: list length, then work-
                                distribution counter, of each launch     */
     uint8_t* tile_fire;     /* [M*TY*TX] scratch of the dense sweep     */
+    int32_t* tile_first;    /* [M][TY][TX] earliest pre-step index at which a cell of the
+                               tile ignited (-1: initial or injected fire), FC_T_NEVER
+                               if none: no cell of the tile has t_ign < tile_first.  The
+                               loss kernels skip tiles with no ignition before an
+                               observation step.  May be NULL (no skipping). */
     int32_t max_steps;
     int32_t pad_;
 } fc_state;

@@ -59,7 +59,8 @@ class FcState(C.Structure):
     _fields_ = [("burn0", C.c_void_p), ("burn1", C.c_void_p), ("burned", C.c_void_p),
                 ("acc", C.c_void_p), ("t_ign", C.c_void_p), ("jac", C.c_void_p),
                 ("flags", C.c_void_p), ("counters", C.c_void_p), ("tile_list", C.c_void_p),
-                ("list_count", C.c_void_p), ("tile_fire", C.c_void_p), ("max_steps", C.c_int32),
+                ("list_count", C.c_void_p), ("tile_fire", C.c_void_p), ("tile_first", C.c_void_p),
+                ("max_steps", C.c_int32),
                 ("pad_", C.c_int32)]
 
 

@@ -252,6 +252,7 @@ class FireBatch:
         self.tile_list = torch.empty((3, ntiles), dtype=torch.int32, device=dev)
         self.list_count = torch.zeros((2 * (self.max_steps + 3),), dtype=torch.int32, device=dev)
         self.tile_fire = torch.zeros((ntiles,), dtype=torch.uint8, device=dev)
+        self.tile_first = torch.full((ntiles,), L.T_NEVER, dtype=torch.int32, device=dev)
         self._mode = None  # sweep mode since reset (activity lists vs dense rescans)
         self.params = torch.zeros((self.m, L.NPARAM), dtype=torch.float64, device=dev)
         self.seeds = torch.zeros((self.m,), dtype=torch.int64, device=dev)
@@ -279,6 +280,7 @@ class FireBatch:
         s.flags, s.counters = L.ptr(self.flags), L.ptr(self.counters)
         s.tile_list, s.list_count = L.ptr(self.tile_list), L.ptr(self.list_count)
         s.tile_fire = L.ptr(self.tile_fire)
+        s.tile_first = L.ptr(self.tile_first)
         s.max_steps = self.max_steps
         return s
 
