@@ -616,3 +616,45 @@ def test_ensemble_runner_host_api_matches_device_batch():
     np.testing.assert_array_equal(out.burned, bd.cpu().numpy())
     np.testing.assert_array_equal(out.accumulator, b.acc.cpu().numpy())
     np.testing.assert_array_equal(out.series, b.series())
+
+
+def test_loss_tile_skipping_matches_full_scan():
+    """fc_loss_grad's tile-skipping path (closed forms for tiles with no fire
+    before an observation step) equals the full per-row scan (tile_first
+    forced to -1: every tile read), for shared and per-member targets."""
+    n, m, steps = 200, 3, 60
+    env = S.make_environment(n, seed=6)
+    dl = F.DeviceLandscape.from_environment(env)
+    b = F.FireBatch((n, n), m, max_steps=steps, with_jacobian=True)
+    b.set_params(np.array([F.pack_params(0.045, 0.131, 0.078, p, 0.3) for p in (0.5, 0.6, 0.7)]))
+    b.set_seeds([1, 2, 3])
+    b.reset(S.center_ignition(n))
+    b.run(dl, steps, attach=[True] * steps)
+    rng = np.random.default_rng(2)
+    tg = torch.zeros((3, n, n), dtype=torch.uint8)
+    tg[0, 90:110, 95:120] = 1
+    tg[1, 80:125, 85:130] = 1
+    tg[2] = torch.from_numpy((rng.random((n, n)) < 0.02).astype(np.uint8))
+    obs = [20, 40, 60]
+    loss, crop, grad, _ = b.loss_grad(tg, obs)
+    saved = b.tile_first.clone()
+    b.tile_first.fill_(-1)
+    loss_f, crop_f, grad_f, _ = b.loss_grad(tg, obs)
+    b.tile_first.copy_(saved)
+    np.testing.assert_array_equal(crop.cpu().numpy(), crop_f.cpu().numpy())
+    np.testing.assert_allclose(loss.cpu().numpy(), loss_f.cpu().numpy(), rtol=1e-12)
+    np.testing.assert_allclose(grad.cpu().numpy(), grad_f.cpu().numpy(), rtol=1e-10, atol=1e-18)
+    # per-member targets take the row path; member 0's row equals the shared result
+    tgm = tg[:, None].expand(3, m, n, n).contiguous()
+    loss_m, _, grad_m, _ = b.loss_grad(tgm, obs)
+    np.testing.assert_allclose(loss_m.cpu().numpy(), loss.cpu().numpy(), rtol=1e-12)
+    np.testing.assert_allclose(grad_m.cpu().numpy(), grad.cpu().numpy(), rtol=1e-10, atol=1e-18)
+    # and the oracle agrees (fp64 reference loss of member 0's accumulator)
+    acc0 = b.acc[0].double().cpu().numpy()
+    t0 = b.t_ign[0].cpu().numpy()
+    tot = 0.0
+    for s_, o in enumerate(obs):
+        x = np.where(t0 < o, acc0, 0.0)
+        bce, mse, _, _ = O.combined_loss(x, tg[s_].numpy())
+        tot += bce + mse
+    assert math.isclose(float(loss[0, 0]), tot, rel_tol=1e-10)
