@@ -134,7 +134,9 @@ size_t fc_loss_workspace_bytes(const fc_grid* g, int32_t n_targets);
 /* -------------------------------------------------------------- state --- */
 /* new_fire_state (model.py:180-200) for every member: init is uint8 [M][H][W]
  * (member_stride = H*W) or one [H][W] mask broadcast (member_stride = 0).
- * t0 = pre-step index of the initial state.  Zeroes jac/counters. */
+ * t0 = pre-step index of the initial state.  Zeroes the counters.  jac is
+ * not cleared: every ignition writes its J (zero on unattached steps) and J
+ * is defined only where t_ign marks an ignition during the run. */
 int fc_state_init(const fc_grid* g, const fc_state* s, const uint8_t* init,
                   int64_t member_stride, int32_t t0, fc_stream_t stream);
 

@@ -82,14 +82,16 @@ def backward_params(tape: Tape, dl_dacc, norm_c: float) -> np.ndarray:
     from .device import FireBatch  # noqa: F401  (lib loaded by the batch)
     gt = torch.as_tensor(g, dtype=torch.float64).to(tape.jac.device) if not torch.is_tensor(g) \
         else g.to(tape.jac.device)
-    out = _contract(tape.jac, gt)
+    # a bound run's plane is valid where its cells ignited (t_ign gates it)
+    tig = tape._batch.t_ign[0] if tape._batch is not None else None
+    out = _contract(tape.jac, gt, tig)
     # chain_k carries the explicit factor c (tape.py:134-140): rescale when
     # the caller's constant differs from the forward's
     scale = float(norm_c) / tape.norm_c if tape.norm_c else 1.0
     return out * scale
 
 
-def _contract(jac: torch.Tensor, g: torch.Tensor) -> np.ndarray:
+def _contract(jac: torch.Tensor, g: torch.Tensor, t_ign: Optional[torch.Tensor] = None) -> np.ndarray:
     import ctypes as C
     from . import _lib as L
     h, w = jac.shape[:2]
@@ -97,7 +99,7 @@ def _contract(jac: torch.Tensor, g: torch.Tensor) -> np.ndarray:
     st = L.FcState()
     st.jac = L.ptr(jac)
     st.acc = 0
-    st.t_ign = 0
+    st.t_ign = 0 if t_ign is None else L.ptr(t_ign)
     gg = g.contiguous()
     ws = torch.empty((max(L.lib().fc_loss_workspace_bytes(C.byref(grid), 1), 4096),),
                      dtype=torch.uint8, device=jac.device)

@@ -658,3 +658,31 @@ def test_loss_tile_skipping_matches_full_scan():
         bce, mse, _, _ = O.combined_loss(x, tg[s_].numpy())
         tot += bce + mse
     assert math.isclose(float(loss[0, 0]), tot, rel_tol=1e-10)
+
+
+def test_reused_batch_gradients_match_fresh_batch():
+    """reset() does not clear the Jacobian plane (every ignition writes its J,
+    zero on unattached steps): a batch reused after a larger fire gives the
+    same loss/gradients and contraction as a fresh one, with partial attach."""
+    n, steps = 128, 40
+    env = S.make_environment(n, seed=8)
+    dl = F.DeviceLandscape.from_environment(env)
+    attach = [(k % 3) == 0 for k in range(steps)]
+    tg = torch.zeros((1, n, n), dtype=torch.uint8)
+    tg[0, 50:80, 50:80] = 1
+
+    def run(b, seed, ph):
+        b.set_params(F.pack_params(0.045, 0.131, 0.078, ph, 0.3))
+        b.set_seeds([seed])
+        b.reset(S.center_ignition(n))
+        b.run(dl, steps, attach=attach)
+        loss, _, grad, _ = b.loss_grad(tg, [steps])
+        g = torch.ones((1, n, n), dtype=torch.float64, device="cuda") * 1e-3
+        return loss.cpu().numpy(), grad.cpu().numpy(), b.contract(g).cpu().numpy()
+
+    used = F.FireBatch((n, n), 1, max_steps=steps, with_jacobian=True)
+    run(used, 1, 0.9)              # a large fire first: J written over a wide area
+    got = run(used, 2, 0.4)        # then a small one on the same planes
+    want = run(F.FireBatch((n, n), 1, max_steps=steps, with_jacobian=True), 2, 0.4)
+    for a_, b_ in zip(got, want):
+        np.testing.assert_array_equal(a_, b_)
