@@ -105,7 +105,7 @@ typedef struct {
     int32_t* tile_list;     /* [3][M*TY*TX] rotating active-tile lists  */
     int32_t* list_count;    /* [2][max_steps+3]: list length, then work-
                                distribution counter, of each launch     */
-    uint8_t* tile_fire;     /* [M*TY*TX] scratch of the dense sweep     */
+    uint8_t* tile_fire;     /* reserved (unused since the fused dense scan; may be NULL) */
     int32_t* tile_first;    /* [M][TY][TX] earliest pre-step index at which a cell of the
                                tile ignited (-1: initial or injected fire), FC_T_NEVER
                                if none: no cell of the tile has t_ign < tile_first.  The

@@ -329,10 +329,11 @@ class FireBatch:
 
     def run(self, land: DeviceLandscape, nsteps: int, *, attach: Optional[Sequence[bool]] = None,
             rng: str = "splitmix", draws: Optional[torch.Tensor] = None, skip_inactive: bool = True,
-            window: int = 8, wind_schedule: Optional[torch.Tensor] = None, shard=None,
+            window: Optional[int] = None, wind_schedule: Optional[torch.Tensor] = None, shard=None,
             stream=None):
         """Advance every member nsteps steps from the current pre-step index,
-        `window` steps per kernel launch (temporal blocking; 1, 4, 8, 16).
+        `window` steps per kernel launch (temporal blocking; 1, 4, 8, 16;
+        default 16 for one or two members, else 8).
         wind_schedule: optional fp64 (max_steps, 4) device tensor of per-step
         {alpha, beta, gamma_deg, 0} (see wind_ramp_schedule)."""
         if nsteps < 0:
@@ -352,6 +353,10 @@ class FireBatch:
             if draws is None or tuple(draws.shape) != (nsteps, self.m, 2, self.h, self.w):
                 raise ValueError("inject mode needs draws of shape (nsteps, M, 2, H, W)")
             draws = draws.to(self.device, torch.float64).contiguous()
+        if window is None:
+            # one or two members are latency-bound: longer windows halve the
+            # launches; ensembles are throughput-bound: shorter halos
+            window = 16 if self.m <= 2 else 8
         if window not in (1, 4, 8, 16):
             raise ValueError("window must be 1, 4, 8 or 16")
         if self._mode is not None and self._mode != bool(skip_inactive):

@@ -41,7 +41,7 @@ def main():
         ev[0].record()
         b.reset(init)
         ev[1].record()
-        b.run(dl, T, attach=att, wind_schedule=sched)
+        b.run(dl, T, attach=att, wind_schedule=sched, window=int(os.environ.get("WINDOW", 8)))
         ev[2].record()
         loss, _, grad, _ = b.loss_grad(targets, [50, 100, 150, 200])
         ev[3].record()
