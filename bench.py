@@ -650,14 +650,15 @@ def bench_dense(dev, peak):
             sms = np.array([a.elapsed_time(c) for a, c in evs[2:]])
             tiles = n * n // 1024
             live = int(b.list_count[b.q].item())
-            sbytes = 128.0 * tiles + tiles + 128.0 * (tiles - live)  # plane read, flags, zero writes
+            sbytes = 128.0 * tiles + 128.0 * (tiles - live)  # plane read + quiet tiles' zero writes
             ach_s = sbytes / (sms.mean() / 1e3) / 1e9
             out["dense"]["activity_scan"] = {"avg_us": float(1e3 * sms.mean()),
                                              "bytes": sbytes, "achieved_GBps": ach_s,
                                              "frac_of_peak": ach_s / peak, "live_tiles": live}
         del b
-    out["note"] = ("dense = every launch rescans the whole domain (fc_activity_scan: the burning "
-                   "plane read once, quiet tiles' next state written as zeros = 256 B per 32x32 "
+    out["note"] = ("dense = every launch rescans the whole domain (fc_activity_scan, one fused "
+                   "kernel: the burning plane read once, quiet tiles' next state written as zeros "
+                   "= 256 B per 32x32 "
                    "tile per launch = 0.25/K B per cell-update) and advances the live tiles; "
                    "skip = incremental activity lists.  The SURVEY's 18 B/cell-update fp32-field "
                    "design would cap a dense sweep at peak/18 = 3.6e11 cu/s")

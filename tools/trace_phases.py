@@ -59,11 +59,19 @@ def main():
     act = tr[:, 0, 0, 0] != 0
     tr = tr[act]
     print("CTAs traced", int(act.sum()))
-    first = tr[:, 0, :, 0]
-    first = first[first > 0]
-    last = tr[:, :, :, 2].max()
-    print(f"span first step start -> last item end: {last - first.min():.0f} cycles "
-          f"({(last - first.min()) / 1965:.1f} us at 1965 MHz)")
+    # per-CTA chain: first step start -> last recorded item end (first group)
+    spans = []
+    for c in range(tr.shape[0]):
+        st0 = tr[c, 0, :, 0]
+        st0 = st0[st0 > 0]
+        ends = tr[c, :, :, 2]
+        ends = ends[ends > 0]
+        if len(st0) and len(ends):
+            spans.append(ends.max() - st0.min())
+    spans = np.array(spans)
+    if len(spans):
+        print(f"per-CTA chain cycles: mean {spans.mean():.0f} p50 {np.median(spans):.0f} "
+              f"p90 {np.percentile(spans, 90):.0f} max {spans.max():.0f}")
     for s_ in range(8):
         st = tr[:, s_]  # (cta, warp, 4)
         ok = (st[:, :, 1] != 0).all(1) & (st[:, :, 2] != 0).all(1)
