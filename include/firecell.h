@@ -37,7 +37,10 @@
  *   activity      flags int32 [M][TY][TX] = last pre-step index at which the
  *                 tile must be visited; tile_list int32 [3][M*TY*TX] rotating
  *                 compacted lists of tiles active at steps t, t+1, t+2 with
- *                 list_count int32 [2][max_steps+3] (zeroed by fc_state_init).
+ *                 list_count int32 [2 (max_steps+3) + 1] (zeroed by fc_state_init):
+ *                 list lengths, per-launch work counters, and last the
+ *                 neighbour-activation distance the current lists were built
+ *                 with (0 = full 3x3 tile neighbourhoods).
  *   params        fp64 [M][8] = {c1, c2, a, p_h, p_continue, norm_c, 0, 0}.
  */
 #ifndef FIRECELL_H
@@ -103,9 +106,11 @@ typedef struct {
     int32_t* flags;         /* [M][TY][TX] last pre-step index active   */
     int32_t* counters;      /* [M][max_steps][FC_NCOUNTER]              */
     int32_t* tile_list;     /* [3][M*TY*TX] rotating active-tile lists  */
-    int32_t* list_count;    /* [2][max_steps+3]: list length, then work-
-                               distribution counter, of each launch     */
-    uint8_t* tile_fire;     /* reserved (unused since the fused dense scan; may be NULL) */
+    int32_t* list_count;    /* [2 (max_steps+3) + 1]: list length, then work-
+                               distribution counter, of each launch; last the
+                               neighbour-activation distance of the lists */
+    uint8_t* tile_fire;     /* [M][TY][TX] per-tile work estimate (log2), written by
+                               the step kernel; orders ensemble lists (may be NULL) */
     int32_t* tile_first;    /* [M][TY][TX] earliest pre-step index at which a cell of the
                                tile ignited (-1: initial or injected fire), FC_T_NEVER
                                if none: no cell of the tile has t_ign < tile_first.  The

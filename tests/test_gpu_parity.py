@@ -302,9 +302,11 @@ def test_temporal_blocking_and_sweep_modes_bit_identical(attach):
     split runs must all give the same bytes (draws are keyed per cell)."""
     h, w, steps = 150, 97, 45
     runs = []
+    # the last case grows the window between runs (4 -> 16 -> 8): neighbour
+    # activation built for a shorter window is widened before the longer one
     for window, skip, split in [(1, True, None), (4, True, None), (8, True, None),
                                 (16, True, None), (8, False, None), (16, False, None),
-                                (8, True, (7, 30))]:
+                                (8, True, (7, 30)), ((4, 16, 8), True, (9, 25))]:
         env = S.make_environment(h, w, seed=12)
         dl = F.DeviceLandscape.from_environment(env)
         b = F.FireBatch((h, w), 2, max_steps=steps, with_jacobian=attach)
@@ -316,8 +318,9 @@ def test_temporal_blocking_and_sweep_modes_bit_identical(attach):
             b.run(dl, steps, attach=att, window=window, skip_inactive=skip)
         else:
             cuts = [0, *split, steps]
-            for a0, a1 in zip(cuts[:-1], cuts[1:]):
-                b.run(dl, a1 - a0, attach=att[a0:a1], window=window, skip_inactive=skip)
+            wins = window if isinstance(window, tuple) else (window,) * (len(cuts) - 1)
+            for a0, a1, wn in zip(cuts[:-1], cuts[1:], wins):
+                b.run(dl, a1 - a0, attach=att[a0:a1], window=wn, skip_inactive=skip)
         bu, bd = b.unpack()
         runs.append((bu, bd, b.acc.clone(), b.t_ign.clone(),
                      None if b.jac is None else b.jac.clone(), b.series()))
