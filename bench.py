@@ -375,6 +375,7 @@ def run_ours(args):
         extras["calibration"] = bench_calibration(dev)
         extras["fig6_sweep"] = bench_fig6_sweep(dev)
         extras["dense_probe"] = bench_dense(dev, peak)
+        extras["c3_single_gpu"] = bench_c3_full(dev)
     cpu = None
     if rank == 0 and world == 1:
         cores = os.cpu_count() or 1
@@ -594,6 +595,42 @@ def bench_fig6_sweep(dev, sizes=(200, 1000, 2000, 4000, 8000, 14000), steps=300)
     return {"steps": steps, "rows": rows,
             "paper": "PyTorchFire: <1 s for maps <1200 (RTX 4090), <=1500 (A800); <60 s at 14000 "
                      "on 'a more advanced GPU'; CPU 300 steps at 1000^2 ~30 s (PAPER.md:456-467)"}
+
+
+def bench_c3_full(dev, steps=1000):
+    """Config 3 at its full length on one GPU: 16384^2, 8 random 5x5
+    ignitions, sigma x32 env, 1000 steps, activity-list sweep, with k = 1
+    (one step per launch, no temporal blocking), k = 4 and k = 8 fused
+    steps.  Device time of the whole run (reset included)."""
+    import torch
+
+    import paper_2502_18738_b200 as F
+    from paper_2502_18738_b200 import synthetic as S
+    n = 16384
+    e = S.make_environment_torch(n, n, seed=3, device=dev)
+    dl = F.DeviceLandscape.from_elevation(e["elevation"], e["wind_speed"], e["wind_direction"],
+                                          e["canopy"], e["density"], device=dev)
+    del e
+    init = torch.as_tensor(S.random_blocks(n, n, 8, 5, seed=3).astype(np.uint8), device=dev)
+    b = F.FireBatch((n, n), 1, max_steps=steps, device=dev)
+    b.set_params(F.pack_params(0.045, 0.131, 0.078, 0.58, 0.3))
+    b.set_seeds([3])
+    out = {"grid": [n, n], "steps": steps, "ignitions": "8 random 5x5 blocks (seed 3)"}
+    for k in (1, 4, 8):
+        b.reset(init)
+        b.run(dl, 2 * k, window=k)  # warm-up
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        b.reset(init)
+        b.run(dl, steps, window=k)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        out[f"k{k}"] = {"ms": ms, "cell_updates_per_s": n * n * steps / (ms / 1e3)}
+    ser = b.series()
+    out["affected_final"] = int(ser[0, -1].sum())
+    return out
 
 
 def bench_dense(dev, peak):
