@@ -689,3 +689,27 @@ def test_reused_batch_gradients_match_fresh_batch():
     want = run(F.FireBatch((n, n), 1, max_steps=steps, with_jacobian=True), 2, 0.4)
     for a_, b_ in zip(got, want):
         np.testing.assert_array_equal(a_, b_)
+
+
+@pytest.mark.parametrize("rng", ["splitmix", "philox"])
+def test_ordered_ensemble_lists_match_dense_sweep(rng):
+    """Ensembles (>= 4 members) order each launch's activity list by work
+    estimate and activate neighbours by distance; the result must equal the
+    dense sweep byte for byte (attached, both RNGs), and for the keyed
+    SplitMix draws a member must equal the CPU oracle."""
+    h, w, steps, M = 190, 170, 70, 6
+    outs = []
+    for skip in (True, False):
+        _, arr, p, init, b = _oracle_vs_device(h, w, steps, 21, True, members=M, skip=skip,
+                                               rng=rng)
+        outs.append(b)
+    a, d = outs
+    assert torch.equal(a.planes, d.planes)
+    assert torch.equal(a.acc, d.acc) and torch.equal(a.t_ign, d.t_ign)
+    assert torch.equal(a.jac, d.jac)
+    assert np.array_equal(a.series(), d.series())
+    if rng == "splitmix":
+        res = O.run(**arr, params=p, init=init, steps=steps, seed=21 + 4,
+                    attach_steps=range(1, steps + 1), threads=4)
+        bu, bd = (x.bool().cpu().numpy() for x in a.unpack())
+        assert np.array_equal(bu[4], res.burning) and np.array_equal(bd[4], res.burned)
