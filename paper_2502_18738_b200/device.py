@@ -316,9 +316,8 @@ class FireBatch:
             raise ValueError(f"initial fire mask must be 2-D or (M,H,W), got {tuple(m8.shape)}")
         # initial burning counts stay on the device (no host sync inside a
         # timed or captured sequence); series() reads them when asked
-        if not torch.cuda.is_current_stream_capturing():
-            cnt = (m8 != 0).reshape(-1, self._hw).sum(1, dtype=torch.int64)
-            self._init_burning_dev = cnt.expand(self.m) if m8.dim() == 2 else cnt
+        cnt = (m8 != 0).reshape(-1, self._hw).sum(1, dtype=torch.int64)
+        self._init_burning_dev.copy_(cnt.expand(self.m) if m8.dim() == 2 else cnt)
         self._init_mask = m8.contiguous()
         st = self.struct()
         L.check(L.lib().fc_state_init(C.byref(self.grid), C.byref(st), L.ptr(self._init_mask),

@@ -47,6 +47,7 @@ class EnsembleRunner:
         self.in_params = _pinned((self.m, 8), torch.float64)
         self.in_seeds = _pinned((self.m,), torch.int64)
         self.copy_stream = torch.cuda.Stream(device=dev)
+        self._graph = None  # CUDA graph of the device part (landscape, reset, run, unpack)
         self.h2d_bytes = self.env_dev.numel() * 4 + self.init_dev.numel()
         self.d2h_bytes = (self.out_b.numel() * 2 + self.out_acc.numel() * 4
                           + self.m * self.steps * 4 * 4)
@@ -62,24 +63,25 @@ class EnsembleRunner:
         st.wait_stream(self.copy_stream)  # the previous call's accumulator copy is done
         self.env_dev.copy_(env_host, non_blocking=True)
         self.init_dev.copy_(init_host, non_blocking=True)
-        e = self.env_dev
-        land = DeviceLandscape.from_elevation(e[0], e[1], e[2], e[3], e[4],
-                                              cell_side=self.cell_side, device=self.dev)
         self.in_params.numpy()[:] = np.array([pack_params(*p, norm_c) for p in params],
                                              dtype=np.float64).reshape(self.m, -1)
         sd = [_u64_to_i64(v) for v in np.atleast_1d(np.asarray(seeds, dtype=object))]
         self.in_seeds.numpy()[:] = sd * self.m if len(sd) == 1 else sd
         self.batch.params.copy_(self.in_params, non_blocking=True)
         self.batch.seeds.copy_(self.in_seeds, non_blocking=True)
-        self.batch.reset(self.init_dev)
-        self.batch.run(land, self.steps, rng=self.rng)
-        # the accumulator leaves on a side stream while the states unpack
+        # device part as one CUDA graph (built on the first call): the
+        # landscape preparation, reset, the window launches and the unpack
+        if self._graph is None:
+            from .device import CapturedSequence
+            self._graph = CapturedSequence(self._device_part)
+        self._graph.replay()
+        # the accumulator leaves on a side stream while the states leave here
         done = torch.cuda.Event()
         done.record(st)
         with torch.cuda.stream(self.copy_stream):
             self.copy_stream.wait_event(done)
             self.out_acc.copy_(self.batch.acc, non_blocking=True)
-        b, d = self.batch.unpack()
+        b, d = self._bu, self._bd
         self.out_b.copy_(b, non_blocking=True)
         self.out_d.copy_(d, non_blocking=True)
         self.out_cnt.copy_(self.batch.counters[:, : max(self.steps, 1)], non_blocking=True)
@@ -93,6 +95,15 @@ class EnsembleRunner:
         burned = np.cumsum(cnt[:, :, 1], axis=1)
         return EnsembleResult(self.out_b.numpy(), self.out_d.numpy(), self.out_acc.numpy(),
                               np.stack([burning, burned], axis=-1))
+
+    def _device_part(self):
+        e = self.env_dev
+        land = DeviceLandscape.from_elevation(e[0], e[1], e[2], e[3], e[4],
+                                              cell_side=self.cell_side, device=self.dev)
+        self._land = land  # keeps the graph's landscape buffers referenced
+        self.batch.reset(self.init_dev)
+        self.batch.run(land, self.steps, rng=self.rng)
+        self._bu, self._bd = self.batch.unpack()
 
 
 class EnsembleCalibrator:

@@ -37,6 +37,9 @@ def main():
         b.reset(init)
         b.run(dl, 500, window=window)
     print(os.environ.get("FIRECELL_SO", "default"), "window", window, "c1 ms/run %.3f" % timeit(c1))
+    if os.environ.get("AB_GRAPH"):
+        g = F.CapturedSequence(c1)
+        print("c1 graph replay ms/run %.3f" % timeit(g.replay))
     n = 1024
     env2 = S.make_environment(n, seed=2)
     dl2 = F.DeviceLandscape.from_environment(env2)
