@@ -182,3 +182,90 @@ def make_environment_torch(h: int, w: int, *, seed: int = 0, sigma_elev: float =
 
     return dict(elevation=elev.float(), wind_speed=speed.float(), wind_direction=direction,
                 canopy=cat(4, VEG_VALUES), density=cat(5, DEN_VALUES))
+
+
+# ----------------------------------------------- named reference landscapes
+# The generator kinds the reference CLI and tests use (pyrocell/synthetic.py:
+# 13-126): host fp64 Landscapes with (H, W, 3, 3) slope grids.
+def _box_smooth(grid: np.ndarray, passes: int) -> np.ndarray:
+    """passes x 3x3 box mean with edge clamping (synthetic.py:13-23); the
+    nine shifted views are summed in row-major offset order."""
+    out = np.asarray(grid, dtype=np.float64)
+    h, w = out.shape
+    for _ in range(passes):
+        p = np.pad(out, 1, mode="edge")
+        acc = np.zeros_like(out)
+        for dr in range(3):
+            for dc in range(3):
+                acc += p[dr:dr + h, dc:dc + w]
+        out = acc / 9.0
+    return out
+
+
+def _dome(size: int, height_m: float) -> np.ndarray:
+    t = np.linspace(-1.0, 1.0, size)
+    x, y = np.meshgrid(t, t)
+    return height_m * np.exp(-2.0 * (x * x + y * y))
+
+
+def _land(speed, direction, altitude, canopy, density, cell_side, slope_sign):
+    from .data_io import slope_from_altitude
+    from .model import Landscape
+    size = np.shape(canopy)[0]
+    full = lambda v: np.full((size, size), float(v)) if np.isscalar(v) else np.asarray(v, np.float64)
+    slope = (np.zeros((size, size, 3, 3)) if altitude is None
+             else slope_from_altitude(altitude, cell_side, slope_sign))
+    return Landscape(wind_speed=full(speed), wind_direction=full(direction), slope=slope,
+                     canopy=full(canopy), density=full(density), cell_side=cell_side)
+
+
+def flat_landscape(size: int, cell_side: float = 30.0):
+    """Windless plain, neutral vegetation."""
+    z = np.zeros((size, size))
+    return _land(0.0, 0.0, None, z, z, cell_side, "downhill-positive")
+
+
+def hill_landscape(size: int, cell_side: float = 30.0, slope_sign: str = "downhill-positive"):
+    """Dome of 8 cell sides, 3 m/s toward 45 degrees."""
+    z = np.zeros((size, size))
+    return _land(3.0, 45.0, _dome(size, 8.0 * cell_side), z, z, cell_side, slope_sign)
+
+
+def valley_landscape(size: int, cell_side: float = 30.0, slope_sign: str = "downhill-positive"):
+    """Inverted dome, 3 m/s toward 225 degrees."""
+    z = np.zeros((size, size))
+    return _land(3.0, 225.0, -_dome(size, 8.0 * cell_side), z, z, cell_side, slope_sign)
+
+
+def windy_landscape(size: int, cell_side: float = 30.0, slope_sign: str = "downhill-positive"):
+    """Gentle dome (2 cell sides), 10 m/s toward 30 degrees, damped
+    vegetation (canopy = density = -0.45)."""
+    damp = np.full((size, size), -0.45)
+    return _land(10.0, 30.0, _dome(size, 2.0 * cell_side), damp, damp, cell_side, slope_sign)
+
+
+def random_landscape(size: int, seed: int, cell_side: float = 30.0,
+                     slope_sign: str = "downhill-positive"):
+    """Box-smoothed random terrain, wind and vegetation; draws in the order
+    altitude, speed, direction, canopy, density from default_rng(seed)."""
+    rng = np.random.default_rng(seed)
+    draw = lambda lo, hi: rng.uniform(lo, hi, (size, size))
+    altitude = _box_smooth(draw(0.0, 6.0 * cell_side), 3)
+    speed = np.clip(_box_smooth(draw(0.0, 6.0), 2), 0.0, None)
+    direction = _box_smooth(draw(0.0, 360.0), 2) % 360.0
+    canopy = np.clip(_box_smooth(draw(-0.4, 0.4), 2), -1.0, None)
+    density = np.clip(_box_smooth(draw(-0.4, 0.4), 2), -1.0, None)
+    return _land(speed, direction, altitude, canopy, density, cell_side, slope_sign)
+
+
+def make_landscape(kind: str, size: int, cell_side: float = 30.0,
+                   slope_sign: str = "downhill-positive"):
+    """flat | hill | valley | windy | random:<seed> (synthetic.py:112-126)."""
+    if kind == "flat":
+        return flat_landscape(size, cell_side)
+    makers = {"hill": hill_landscape, "valley": valley_landscape, "windy": windy_landscape}
+    if kind in makers:
+        return makers[kind](size, cell_side, slope_sign)
+    if kind.startswith("random:"):
+        return random_landscape(size, int(kind.split(":", 1)[1]), cell_side, slope_sign)
+    raise ValueError(f"unknown synthetic landscape {kind!r}")
