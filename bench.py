@@ -355,20 +355,31 @@ def run_ours(args):
                             (env.elevation, env.wind_speed, env.wind_direction, env.canopy,
                              env.density)]).pin_memory()
     init_host = torch.from_numpy(init.astype(np.uint8)).pin_memory()
-    for _ in range(max(1, args.warmup)):
+    for _ in range(max(len(runner.slots), args.warmup)):
         runner(env_host, init_host, params, members)
     barrier()
-    e2e_ms = []
+    # K calls pipelined two deep (EnsembleRunner.submit): call i's results
+    # are read on the host while call i+1 uploads and runs; every call's
+    # H2D and D2H lies inside the timed region, L2 flushed between calls
+    flush()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    prev = None
     for _ in range(args.steps):
         flush()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        runner(env_host, init_host, params, members)
-        e2e_ms.append(1e3 * (time.perf_counter() - t0))
-    e2e_total = allreduce_max(float(sum(e2e_ms)), dev)
+        tk = runner.submit(env_host, init_host, params, members)
+        if prev is not None:
+            res = prev.result()
+            e2e_check = int(res.series[0, -1, 0])  # read the result on the host
+        prev = tk
+    res = prev.result()
+    e2e_check = int(res.series[0, -1, 0])
+    e2e_total = allreduce_max(1e3 * (time.perf_counter() - t0), dev)
     e2e = {"value": cu / (e2e_total / 1e3), "unit": "cell-updates/s",
            "h2d_bytes_per_step": int(runner.h2d_bytes), "d2h_bytes_per_step": int(runner.d2h_bytes),
-           "api": "paper_2502_18738_b200.ensemble.EnsembleRunner (pinned host in/out)"}
+           "api": "paper_2502_18738_b200.ensemble.EnsembleRunner.submit (pinned host in/out, "
+                  "2-deep pipeline: D2H of call i overlaps H2D + kernels of call i+1)",
+           "final_burning_member0": e2e_check}
 
     extras = {}
     if not args.no_extras:

@@ -4,6 +4,14 @@
 each call uploads one landscape (fp32 rasters) and the initial mask, runs M
 members for `steps` steps on the device (libfirecell fc_run) and copies the
 final states, accumulators and per-step counts back to host memory.
+
+Calls can be pipelined: ``submit`` queues one call and returns a ticket
+whose ``result()`` waits for that call's copies.  The runner holds ``depth``
+slots (device buffers, a captured CUDA graph of the device part, pinned
+inputs and outputs each); a call's device->host copies run on their own
+stream, so they overlap the next call's host->device copies (the other PCIe
+direction) and its kernels.  A result's arrays are views of its slot's
+pinned buffers and stay valid until ``depth`` further submissions.
 """
 from __future__ import annotations
 
@@ -28,82 +36,120 @@ def _pinned(shape, dtype):
     return torch.empty(shape, dtype=dtype, pin_memory=True)
 
 
+class _Slot:
+    """One pipeline stage: device state + graph + pinned staging."""
+
+    def __init__(self, runner: "EnsembleRunner", device):
+        r = runner
+        self.batch = FireBatch((r.h, r.w), r.m, max_steps=max(r.steps, 1), device=device)
+        dev = self.batch.device
+        self.env_dev = torch.empty((5, r.h, r.w), dtype=torch.float32, device=dev)
+        self.init_dev = torch.empty((r.h, r.w), dtype=torch.uint8, device=dev)
+        self.out_b = _pinned((r.m, r.h, r.w), torch.uint8)
+        self.out_d = _pinned((r.m, r.h, r.w), torch.uint8)
+        self.out_acc = _pinned((r.m, r.h, r.w), torch.float32)
+        self.out_cnt = _pinned((r.m, max(r.steps, 1), 4), torch.int32)
+        self.out_init = _pinned((r.m,), torch.int64)
+        self.in_params = _pinned((r.m, 8), torch.float64)
+        self.in_seeds = _pinned((r.m,), torch.int64)
+        self.uploaded = None   # event: this slot's pinned inputs have been read
+        self.copied = None     # event: this slot's outputs are in host memory
+        self.graph = None
+        self.runner = r
+
+    def device_part(self):
+        r, e = self.runner, self.env_dev
+        land = DeviceLandscape.from_elevation(e[0], e[1], e[2], e[3], e[4],
+                                              cell_side=r.cell_side, device=self.batch.device)
+        self._land = land  # keeps the graph's landscape buffers referenced
+        self.batch.reset(self.init_dev)
+        self.batch.run(land, r.steps, rng=r.rng)
+        self.bu, self.bd = self.batch.unpack()
+
+
+class EnsembleTicket:
+    """A submitted call; result() blocks until its outputs are on the host."""
+
+    def __init__(self, slot: _Slot, steps: int):
+        self.slot, self.steps, self.event = slot, steps, slot.copied
+
+    def done(self) -> bool:
+        return self.event.query()
+
+    def result(self) -> EnsembleResult:
+        self.event.synchronize()
+        s = self.slot
+        cnt = s.out_cnt.numpy()[:, : self.steps].astype(np.int64)
+        burning = s.out_init.numpy()[:, None] + np.cumsum(cnt[:, :, 0] - cnt[:, :, 1], axis=1)
+        burned = np.cumsum(cnt[:, :, 1], axis=1)
+        return EnsembleResult(s.out_b.numpy(), s.out_d.numpy(), s.out_acc.numpy(),
+                              np.stack([burning, burned], axis=-1))
+
+
 class EnsembleRunner:
     def __init__(self, shape, members: int, steps: int, *, cell_side: float = 30.0,
-                 rng: str = "splitmix", device=None):
+                 rng: str = "splitmix", depth: int = 2, device=None):
         self.h, self.w = shape
         self.m, self.steps, self.rng = int(members), int(steps), rng
         self.cell_side = cell_side
-        self.batch = FireBatch(shape, members, max_steps=max(steps, 1), device=device)
-        dev = self.batch.device
-        self.dev = dev
-        self.env_dev = torch.empty((5, self.h, self.w), dtype=torch.float32, device=dev)
-        self.init_dev = torch.empty((self.h, self.w), dtype=torch.uint8, device=dev)
-        self.out_b = _pinned((self.m, self.h, self.w), torch.uint8)
-        self.out_d = _pinned((self.m, self.h, self.w), torch.uint8)
-        self.out_acc = _pinned((self.m, self.h, self.w), torch.float32)
-        self.out_cnt = _pinned((self.m, max(steps, 1), 4), torch.int32)
-        self.out_init = _pinned((self.m,), torch.int64)
-        self.in_params = _pinned((self.m, 8), torch.float64)
-        self.in_seeds = _pinned((self.m,), torch.int64)
-        self.copy_stream = torch.cuda.Stream(device=dev)
-        self._graph = None  # CUDA graph of the device part (landscape, reset, run, unpack)
-        self.h2d_bytes = self.env_dev.numel() * 4 + self.init_dev.numel()
-        self.d2h_bytes = (self.out_b.numel() * 2 + self.out_acc.numel() * 4
+        if depth < 1:
+            raise ValueError("depth must be >= 1")
+        self.slots = [_Slot(self, device) for _ in range(depth)]
+        self.dev = self.slots[0].batch.device
+        self.batch = self.slots[0].batch
+        self.copy_stream = torch.cuda.Stream(device=self.dev)
+        self._next = 0
+        s0 = self.slots[0]
+        self.h2d_bytes = s0.env_dev.numel() * 4 + s0.init_dev.numel()
+        self.d2h_bytes = (s0.out_b.numel() * 2 + s0.out_acc.numel() * 4
                           + self.m * self.steps * 4 * 4)
 
-    def __call__(self, env_host: torch.Tensor, init_host: torch.Tensor, params: Sequence,
-                 seeds: Sequence[int], norm_c: float = DEFAULT_NORM_C,
-                 sync: bool = True) -> EnsembleResult:
-        """env_host: (5, H, W) fp32 (elevation, speed, direction, canopy,
-        density), ideally pinned; init_host: (H, W) uint8/bool;
-        params: per-member (c1, c2, a, p_h, p_continue)."""
-        from .device import _u64_to_i64
+    def submit(self, env_host: torch.Tensor, init_host: torch.Tensor, params: Sequence,
+               seeds: Sequence[int], norm_c: float = DEFAULT_NORM_C) -> EnsembleTicket:
+        """Queue one call.  env_host: (5, H, W) fp32 (elevation, speed,
+        direction, canopy, density), ideally pinned; init_host: (H, W)
+        uint8/bool; params: per-member (c1, c2, a, p_h, p_continue)."""
+        from .device import CapturedSequence, _u64_to_i64
+        slot = self.slots[self._next]
+        self._next = (self._next + 1) % len(self.slots)
         st = torch.cuda.current_stream(self.dev)
-        st.wait_stream(self.copy_stream)  # the previous call's accumulator copy is done
-        self.env_dev.copy_(env_host, non_blocking=True)
-        self.init_dev.copy_(init_host, non_blocking=True)
-        self.in_params.numpy()[:] = np.array([pack_params(*p, norm_c) for p in params],
+        if slot.uploaded is not None:
+            slot.uploaded.synchronize()        # its pinned inputs are free to refill
+        slot.in_params.numpy()[:] = np.array([pack_params(*p, norm_c) for p in params],
                                              dtype=np.float64).reshape(self.m, -1)
         sd = [_u64_to_i64(v) for v in np.atleast_1d(np.asarray(seeds, dtype=object))]
-        self.in_seeds.numpy()[:] = sd * self.m if len(sd) == 1 else sd
-        self.batch.params.copy_(self.in_params, non_blocking=True)
-        self.batch.seeds.copy_(self.in_seeds, non_blocking=True)
-        # device part as one CUDA graph (built on the first call): the
+        slot.in_seeds.numpy()[:] = sd * self.m if len(sd) == 1 else sd
+        if slot.copied is not None:
+            st.wait_event(slot.copied)         # its device outputs have left
+        slot.env_dev.copy_(env_host, non_blocking=True)
+        slot.init_dev.copy_(init_host, non_blocking=True)
+        slot.batch.params.copy_(slot.in_params, non_blocking=True)
+        slot.batch.seeds.copy_(slot.in_seeds, non_blocking=True)
+        slot.uploaded = torch.cuda.Event()
+        slot.uploaded.record(st)
+        # device part as one CUDA graph per slot (built on its first call):
         # landscape preparation, reset, the window launches and the unpack
-        if self._graph is None:
-            from .device import CapturedSequence
-            self._graph = CapturedSequence(self._device_part)
-        self._graph.replay()
-        # the accumulator leaves on a side stream while the states leave here
-        done = torch.cuda.Event()
-        done.record(st)
-        with torch.cuda.stream(self.copy_stream):
-            self.copy_stream.wait_event(done)
-            self.out_acc.copy_(self.batch.acc, non_blocking=True)
-        b, d = self._bu, self._bd
-        self.out_b.copy_(b, non_blocking=True)
-        self.out_d.copy_(d, non_blocking=True)
-        self.out_cnt.copy_(self.batch.counters[:, : max(self.steps, 1)], non_blocking=True)
-        self.out_init.copy_(self.batch._init_burning_dev, non_blocking=True)
-        self.batch.acc.record_stream(self.copy_stream)
-        if sync:
-            st.synchronize()
-            self.copy_stream.synchronize()
-        cnt = self.out_cnt.numpy()[:, : self.steps].astype(np.int64)
-        burning = self.out_init.numpy()[:, None] + np.cumsum(cnt[:, :, 0] - cnt[:, :, 1], axis=1)
-        burned = np.cumsum(cnt[:, :, 1], axis=1)
-        return EnsembleResult(self.out_b.numpy(), self.out_d.numpy(), self.out_acc.numpy(),
-                              np.stack([burning, burned], axis=-1))
+        if slot.graph is None:
+            slot.graph = CapturedSequence(slot.device_part)
+        slot.graph.replay()
+        computed = torch.cuda.Event()
+        computed.record(st)
+        cs = self.copy_stream
+        with torch.cuda.stream(cs):
+            cs.wait_event(computed)
+            slot.out_b.copy_(slot.bu, non_blocking=True)
+            slot.out_d.copy_(slot.bd, non_blocking=True)
+            slot.out_acc.copy_(slot.batch.acc, non_blocking=True)
+            slot.out_cnt.copy_(slot.batch.counters[:, : max(self.steps, 1)], non_blocking=True)
+            slot.out_init.copy_(slot.batch._init_burning_dev, non_blocking=True)
+            slot.copied = torch.cuda.Event()
+            slot.copied.record(cs)
+        return EnsembleTicket(slot, self.steps)
 
-    def _device_part(self):
-        e = self.env_dev
-        land = DeviceLandscape.from_elevation(e[0], e[1], e[2], e[3], e[4],
-                                              cell_side=self.cell_side, device=self.dev)
-        self._land = land  # keeps the graph's landscape buffers referenced
-        self.batch.reset(self.init_dev)
-        self.batch.run(land, self.steps, rng=self.rng)
-        self._bu, self._bd = self.batch.unpack()
+    def __call__(self, env_host: torch.Tensor, init_host: torch.Tensor, params: Sequence,
+                 seeds: Sequence[int], norm_c: float = DEFAULT_NORM_C) -> EnsembleResult:
+        """One synchronous call (submit + result)."""
+        return self.submit(env_host, init_host, params, seeds, norm_c).result()
 
 
 class EnsembleCalibrator:

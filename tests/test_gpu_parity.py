@@ -621,6 +621,39 @@ def test_ensemble_runner_host_api_matches_device_batch():
     np.testing.assert_array_equal(out.series, b.series())
 
 
+def test_ensemble_runner_pipelined_submits():
+    """submit() tickets (depth-2 slot ring, copies overlapping the next
+    call) return the same results as synchronous calls, per submission."""
+    from paper_2502_18738_b200.ensemble import EnsembleRunner
+    n, m, steps = 128, 2, 40
+    envs = []
+    for k in range(3):
+        env = S.make_environment(n, seed=10 + k)
+        envs.append(torch.stack([torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32))
+                                 for a in (env.elevation, env.wind_speed, env.wind_direction,
+                                           env.canopy, env.density)]).pin_memory())
+    init = torch.from_numpy(S.center_ignition(n).astype(np.uint8))
+    params = [(0.045, 0.131, 0.078, p, 0.3) for p in (0.55, 0.65)]
+    ref = EnsembleRunner((n, n), m, steps, depth=1)
+    want = []
+    for k in range(5):
+        o = ref(envs[k % 3], init, params, [k, k + 7])
+        want.append([a.copy() for a in (o.burning, o.burned, o.accumulator, o.series)])
+    r = EnsembleRunner((n, n), m, steps, depth=2)
+    tickets, got = [], []
+    for k in range(5):
+        tickets.append(r.submit(envs[k % 3], init, params, [k, k + 7]))
+        if k >= 1:
+            o = tickets[k - 1].result()
+            got.append([a.copy() for a in (o.burning, o.burned, o.accumulator, o.series)])
+    o = tickets[-1].result()
+    got.append([a.copy() for a in (o.burning, o.burned, o.accumulator, o.series)])
+    for g, w in zip(got, want):
+        for x, y in zip(g, w):
+            np.testing.assert_array_equal(x, y)
+    assert any(not np.array_equal(want[0][2], w[2]) for w in want[1:])
+
+
 def test_loss_tile_skipping_matches_full_scan():
     """fc_loss_grad's tile-skipping path (closed forms for tiles with no fire
     before an observation step) equals the full per-row scan (tile_first

@@ -30,7 +30,18 @@ def main():
     for _ in range(5):
         r(env_host, init_host, params, list(range(16)))
     print("e2e call ms", (time.perf_counter() - t0) / 5 * 1e3)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    prev = None
+    for _ in range(10):
+        t = r.submit(env_host, init_host, params, list(range(16)))
+        if prev is not None:
+            prev.result()
+        prev = t
+    prev.result()
+    print("e2e pipelined ms per call", (time.perf_counter() - t0) / 10 * 1e3)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(8)]
+    r = r.slots[0]
     b = r.batch
     for rep in range(2):
         torch.cuda.synchronize()
