@@ -376,9 +376,16 @@ def run_ours(args):
     e2e_check = int(res.series[0, -1, 0])
     e2e_total = allreduce_max(1e3 * (time.perf_counter() - t0), dev)
     e2e = {"value": cu / (e2e_total / 1e3), "unit": "cell-updates/s",
-           "h2d_bytes_per_step": int(runner.h2d_bytes), "d2h_bytes_per_step": int(runner.d2h_bytes),
+           "h2d_bytes_per_step": int(runner.h2d_bytes), "d2h_bytes_per_step": int(runner.d2h_bytes(prev)),
+           "d2h_note": "fc_state_export writes the (M,H,W) burning/burned/accumulator result "
+                       "arrays in pinned host memory from the device, only for tiles affected "
+                       "now or written by the slot's previous call (%d of %d tiles); the "
+                       "dense arrays would be %d B" % (prev.exported_tiles(),
+                                                       runner.batch.grid.tiles_x * runner.batch.grid.tiles_y * MEMBERS,
+                                                       runner.d2h_bytes_dense),
            "api": "paper_2502_18738_b200.ensemble.EnsembleRunner.submit (pinned host in/out, "
-                  "2-deep pipeline: D2H of call i overlaps H2D + kernels of call i+1)",
+                  "2-deep pipeline: upload of call i+1, kernels of call i and export of "
+                  "call i-1 on three streams)",
            "final_burning_member0": e2e_check}
 
     extras = {}

@@ -97,9 +97,13 @@ typedef struct {
 } fc_landscape;
 
 typedef struct {
-    uint32_t* burn0;        /* [M][TY][TX][32] burning, even pre-steps  */
-    uint32_t* burn1;        /* [M][TY][TX][32] burning, odd pre-steps   */
-    uint32_t* burned;       /* [M][TY][TX][32]                          */
+    uint32_t* burn0;        /* [M][TY][TX][32] burning, even launch phases */
+    uint32_t* burn1;        /* [M][TY][TX][32] burning, odd launch phases  */
+    uint32_t* burned0;      /* [M][TY][TX][32] burned, even launch phases  */
+    uint32_t* burned1;      /* [M][TY][TX][32] burned, odd launch phases: a
+                               launch reads the halo of neighbouring tiles
+                               from the phase's input buffers while those
+                               tiles' new states go to the output buffers */
     float* acc;             /* [M][H][W]                                */
     int16_t* t_ign;         /* [M][H][W]                                */
     float* jac;             /* [M][H][W][4], may be NULL (no gradients) */
@@ -150,6 +154,24 @@ int fc_state_init(const fc_grid* g, const fc_state* s, const uint8_t* init,
  * burning buffer).  Mirrors FireState.burning / burned (model.py:158-160). */
 int fc_state_unpack(const fc_grid* g, const fc_state* s, int32_t phase, uint8_t* burning,
                     uint8_t* burned, fc_stream_t stream);
+
+/* Export the current state into [M][H][W] result arrays: burning / burned as
+ * uint8 0/1 and the accumulator as fp32 (any may be NULL) -- the same values
+ * fc_state_unpack and the acc plane hold.  The arrays may be pinned host
+ * memory mapped into the device address space (fc_host_device_pointer), so
+ * the kernel writes the results over PCIe without a device staging copy.
+ * written: NULL = every tile is written; else uint8 [M][TY][TX] flags owned
+ * by the destination (zero-initialised together with it): only tiles that are
+ * affected now (tile_first set) or were written by the previous export into
+ * the same destination are written, and the flags are updated.  The caller
+ * keeps the destination's other cells zero.  Replaces the host-side copy of
+ * FireState.burning / burned / accumulator (model.py:148-177) at the end of
+ * run_simulation (kernel.py:525-529). */
+int fc_state_export(const fc_grid* g, const fc_state* s, int32_t phase, uint8_t* burning,
+                    uint8_t* burned, float* acc, uint8_t* written, fc_stream_t stream);
+
+/* Device address of pinned host memory (cudaHostGetDevicePointer). */
+int fc_host_device_pointer(void* host, void** device_ptr);
 
 /* inject_ignitions (kernel.py:405-419) before pre-step t (launch phase
  * `phase`): cells is int32 [n][3] = (member, row, col), all in bounds

@@ -30,7 +30,7 @@ NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", 
 
 # Every symbol include/firecell.h declares (checked by the CPU test suite).
 EXPORTS = ("fc_grid_make", "fc_plane_words", "fc_loss_workspace_bytes", "fc_state_init",
-           "fc_state_unpack", "fc_inject", "fc_run", "fc_mark_ghosts", "fc_activity_scan",
+           "fc_state_unpack", "fc_state_export", "fc_host_device_pointer", "fc_inject", "fc_run", "fc_mark_ghosts", "fc_activity_scan",
            "fc_contract", "fc_loss_grad",
            "fc_loss_dense", "fc_adamw", "fc_uniform_grid", "fc_epoch_seed", "fc_build_fields",
            "fc_landscape_build",
@@ -56,7 +56,8 @@ class FcShard(C.Structure):
 
 
 class FcState(C.Structure):
-    _fields_ = [("burn0", C.c_void_p), ("burn1", C.c_void_p), ("burned", C.c_void_p),
+    _fields_ = [("burn0", C.c_void_p), ("burn1", C.c_void_p), ("burned0", C.c_void_p),
+                ("burned1", C.c_void_p),
                 ("acc", C.c_void_p), ("t_ign", C.c_void_p), ("jac", C.c_void_p),
                 ("flags", C.c_void_p), ("counters", C.c_void_p), ("tile_list", C.c_void_p),
                 ("list_count", C.c_void_p), ("tile_fire", C.c_void_p), ("tile_first", C.c_void_p),
@@ -101,6 +102,8 @@ def lib():
             "fc_loss_workspace_bytes": (C.c_size_t, [G, i32]),
             "fc_state_init": (C.c_int, [G, ST, vp, i64, i32, vp]),
             "fc_state_unpack": (C.c_int, [G, ST, i32, vp, vp, vp]),
+            "fc_state_export": (C.c_int, [G, ST, i32, vp, vp, vp, vp, vp]),
+            "fc_host_device_pointer": (C.c_int, [vp, C.POINTER(vp)]),
             "fc_inject": (C.c_int, [G, ST, vp, i32, i32, i32, vp]),
             "fc_run": (C.c_int, [G, LS, ST, vp, vp, i32, vp, i32, i32, vp, i32, i32, vp, SH,
                                  C.POINTER(i32), vp]),
@@ -158,3 +161,18 @@ def stream_ptr(stream=None) -> int:
 
 def ptr(t) -> int:
     return 0 if t is None else int(t.data_ptr())
+
+
+def device_ptr(t) -> int:
+    """Device address of a CUDA tensor, or of a pinned host tensor mapped
+    into the device address space (fc_host_device_pointer)."""
+    if t is None:
+        return 0
+    if t.is_cuda:
+        return int(t.data_ptr())
+    if not t.is_pinned():
+        raise ValueError("host tensor must be pinned to be written by the device")
+    out = C.c_void_p()
+    check(lib().fc_host_device_pointer(C.c_void_p(t.data_ptr()), C.byref(out)),
+          "fc_host_device_pointer")
+    return int(out.value or 0)

@@ -236,7 +236,7 @@ class FireBatch:
         self.m = int(members)
         self.grid = L.grid(self.h, self.w, self.m)
         words = L.lib().fc_plane_words(C.byref(self.grid))
-        self.planes = torch.empty((3, words), dtype=torch.int32, device=dev)
+        self.planes = torch.empty((4, words), dtype=torch.int32, device=dev)
         hw = self.h * self.w
         self.acc = torch.zeros((self.m, self.h, self.w), dtype=torch.float32, device=dev)
         self.t_ign = torch.empty((self.m, self.h, self.w), dtype=torch.int16, device=dev)
@@ -275,7 +275,8 @@ class FireBatch:
     def struct(self) -> L.FcState:
         s = L.FcState()
         base, stride = self.planes.data_ptr(), self.planes.stride(0) * 4
-        s.burn0, s.burn1, s.burned = base, base + stride, base + 2 * stride
+        s.burn0, s.burn1 = base, base + stride
+        s.burned0, s.burned1 = base + 2 * stride, base + 3 * stride
         s.acc, s.t_ign, s.jac = L.ptr(self.acc), L.ptr(self.t_ign), L.ptr(self.jac)
         s.flags, s.counters = L.ptr(self.flags), L.ptr(self.counters)
         s.tile_list, s.list_count = L.ptr(self.tile_list), L.ptr(self.list_count)
@@ -403,6 +404,27 @@ class FireBatch:
         L.check(L.lib().fc_state_unpack(C.byref(self.grid), C.byref(st), self.q, L.ptr(b),
                                         L.ptr(d), L.stream_ptr(stream)), "fc_state_unpack")
         return b, d
+
+    def export(self, burning, burned, acc, written=None, stream=None):
+        """fc_state_export: the current state into (M, H, W) uint8 / uint8 /
+        fp32 tensors (any may be None), on the device or pinned on the host
+        (written by the kernel over PCIe).  written: None, or a uint8
+        (M, TY, TX) device tensor of per-tile flags kept with a reused
+        destination (zero-initialised with it): only affected tiles and
+        tiles written last time are then touched."""
+        for t, dt in ((burning, torch.uint8), (burned, torch.uint8), (acc, torch.float32)):
+            if t is not None and (t.dtype != dt or tuple(t.shape) != (self.m, self.h, self.w)
+                                  or not t.is_contiguous()):
+                raise ValueError("export destinations must be contiguous (M, H, W) "
+                                 "uint8 / uint8 / float32")
+        if written is not None and (written.dtype != torch.uint8 or not written.is_cuda or
+                                    written.numel() != self.m * self.grid.tiles_y * self.grid.tiles_x):
+            raise ValueError("written must be a uint8 (M, TY, TX) device tensor")
+        st = self.struct()
+        L.check(L.lib().fc_state_export(C.byref(self.grid), C.byref(st), self.q,
+                                        L.device_ptr(burning), L.device_ptr(burned),
+                                        L.device_ptr(acc), L.ptr(written), L.stream_ptr(stream)),
+                "fc_state_export")
 
     def series(self, t0: int = 0, t1: Optional[int] = None) -> np.ndarray:
         """Per-step (burning, burned) counts after each step in [t0, t1)

@@ -6,12 +6,16 @@ members for `steps` steps on the device (libfirecell fc_run) and copies the
 final states, accumulators and per-step counts back to host memory.
 
 Calls can be pipelined: ``submit`` queues one call and returns a ticket
-whose ``result()`` waits for that call's copies.  The runner holds ``depth``
-slots (device buffers, a captured CUDA graph of the device part, pinned
-inputs and outputs each); a call's device->host copies run on their own
-stream, so they overlap the next call's host->device copies (the other PCIe
-direction) and its kernels.  A result's arrays are views of its slot's
-pinned buffers and stay valid until ``depth`` further submissions.
+whose ``result()`` waits for that call's outputs.  The runner holds
+``depth`` slots (device buffers, a captured CUDA graph of the device part,
+pinned inputs and outputs each).  Three streams overlap: uploads of call
+i+1, the kernels of call i, and the export of call i-1 -- fc_state_export
+writes the result arrays in pinned host memory directly from the bit planes,
+touching only tiles that are affected now or were written by the slot's
+previous call (everywhere else the arrays already hold zeros), so the PCIe
+traffic is the fire's footprint, not the grid.  A result's arrays are
+read-only views of its slot's buffers, valid until ``depth`` further
+submissions.
 """
 from __future__ import annotations
 
@@ -37,22 +41,29 @@ def _pinned(shape, dtype):
 
 
 class _Slot:
-    """One pipeline stage: device state + graph + pinned staging."""
+    """One pipeline stage: device state + graph + pinned staging.  The
+    result arrays are pinned host memory the export kernel writes directly
+    (zero-initialised once; per-tile ``written`` flags keep them exact)."""
 
     def __init__(self, runner: "EnsembleRunner", device):
+        from . import _lib as L
         r = runner
         self.batch = FireBatch((r.h, r.w), r.m, max_steps=max(r.steps, 1), device=device)
         dev = self.batch.device
+        g = self.batch.grid
         self.env_dev = torch.empty((5, r.h, r.w), dtype=torch.float32, device=dev)
         self.init_dev = torch.empty((r.h, r.w), dtype=torch.uint8, device=dev)
-        self.out_b = _pinned((r.m, r.h, r.w), torch.uint8)
-        self.out_d = _pinned((r.m, r.h, r.w), torch.uint8)
-        self.out_acc = _pinned((r.m, r.h, r.w), torch.float32)
+        self.out_b = torch.zeros((r.m, r.h, r.w), dtype=torch.uint8, pin_memory=True)
+        self.out_d = torch.zeros((r.m, r.h, r.w), dtype=torch.uint8, pin_memory=True)
+        self.out_acc = torch.zeros((r.m, r.h, r.w), dtype=torch.float32, pin_memory=True)
+        self.written = torch.zeros((r.m, g.tiles_y, g.tiles_x), dtype=torch.uint8, device=dev)
+        self.out_ptrs = [L.device_ptr(t) for t in (self.out_b, self.out_d, self.out_acc)]
         self.out_cnt = _pinned((r.m, max(r.steps, 1), 4), torch.int32)
         self.out_init = _pinned((r.m,), torch.int64)
         self.in_params = _pinned((r.m, 8), torch.float64)
         self.in_seeds = _pinned((r.m,), torch.int64)
         self.uploaded = None   # event: this slot's pinned inputs have been read
+        self.computed = None   # event: this slot's device part has run
         self.copied = None     # event: this slot's outputs are in host memory
         self.graph = None
         self.runner = r
@@ -64,7 +75,18 @@ class _Slot:
         self._land = land  # keeps the graph's landscape buffers referenced
         self.batch.reset(self.init_dev)
         self.batch.run(land, r.steps, rng=r.rng)
-        self.bu, self.bd = self.batch.unpack()
+
+    def export(self, stream):
+        """fc_state_export into the pinned result arrays + the counters."""
+        import ctypes as C
+        from . import _lib as L
+        b = self.batch
+        st = b.struct()
+        L.check(L.lib().fc_state_export(C.byref(b.grid), C.byref(st), b.q, *self.out_ptrs,
+                                        L.ptr(self.written), L.stream_ptr(stream)),
+                "fc_state_export")
+        self.out_cnt.copy_(b.counters[:, : max(self.runner.steps, 1)], non_blocking=True)
+        self.out_init.copy_(b._init_burning_dev, non_blocking=True)
 
 
 class EnsembleTicket:
@@ -82,8 +104,14 @@ class EnsembleTicket:
         cnt = s.out_cnt.numpy()[:, : self.steps].astype(np.int64)
         burning = s.out_init.numpy()[:, None] + np.cumsum(cnt[:, :, 0] - cnt[:, :, 1], axis=1)
         burned = np.cumsum(cnt[:, :, 1], axis=1)
-        return EnsembleResult(s.out_b.numpy(), s.out_d.numpy(), s.out_acc.numpy(),
-                              np.stack([burning, burned], axis=-1))
+        arrays = [s.out_b.numpy(), s.out_d.numpy(), s.out_acc.numpy()]
+        for a in arrays:  # the slot's buffers are reused: callers copy to keep or modify
+            a.flags.writeable = False
+        return EnsembleResult(*arrays, np.stack([burning, burned], axis=-1))
+
+    def exported_tiles(self) -> int:
+        """Tiles the export wrote (after result(); syncs)."""
+        return int(self.slot.written.sum())
 
 
 class EnsembleRunner:
@@ -97,51 +125,76 @@ class EnsembleRunner:
         self.slots = [_Slot(self, device) for _ in range(depth)]
         self.dev = self.slots[0].batch.device
         self.batch = self.slots[0].batch
+        self.upload_stream = torch.cuda.Stream(device=self.dev)
         self.copy_stream = torch.cuda.Stream(device=self.dev)
         self._next = 0
         s0 = self.slots[0]
-        self.h2d_bytes = s0.env_dev.numel() * 4 + s0.init_dev.numel()
-        self.d2h_bytes = (s0.out_b.numel() * 2 + s0.out_acc.numel() * 4
-                          + self.m * self.steps * 4 * 4)
+        self.h2d_bytes = s0.env_dev.numel() * 4 + s0.init_dev.numel() + self.m * (8 + 1) * 8
+        # full-grid equivalent; the export writes only affected tiles
+        self.d2h_bytes_dense = (s0.out_b.numel() * 2 + s0.out_acc.numel() * 4
+                                + self.m * self.steps * 4 * 4)
+
+    def d2h_bytes(self, ticket: EnsembleTicket) -> int:
+        """Bytes one call moved device -> host: the exported tiles (1 + 1 + 4
+        B per cell) and the counters."""
+        g = ticket.slot.batch.grid
+        full_tiles = (self.h // 32) * (self.w // 32) == g.tiles_y * g.tiles_x
+        per_tile = 32 * 32 * 6 if full_tiles else None
+        n = ticket.exported_tiles()
+        if per_tile is None:  # ragged edges: count cells of the written tiles exactly
+            w = ticket.slot.written.to(torch.int64).cpu().numpy()
+            rows = np.minimum(32, self.h - 32 * np.arange(g.tiles_y))[:, None]
+            cols = np.minimum(32, self.w - 32 * np.arange(g.tiles_x))[None, :]
+            cells = int((w * (rows * cols)[None]).sum())
+            return cells * 6 + self.m * (self.steps * 16 + 8)
+        return n * per_tile + self.m * (self.steps * 16 + 8)
 
     def submit(self, env_host: torch.Tensor, init_host: torch.Tensor, params: Sequence,
                seeds: Sequence[int], norm_c: float = DEFAULT_NORM_C) -> EnsembleTicket:
         """Queue one call.  env_host: (5, H, W) fp32 (elevation, speed,
         direction, canopy, density), ideally pinned; init_host: (H, W)
-        uint8/bool; params: per-member (c1, c2, a, p_h, p_continue)."""
+        uint8/bool; params: per-member (c1, c2, a, p_h, p_continue).
+
+        Streams: uploads on upload_stream (overlapping the previous call's
+        kernels), the device part (one CUDA graph) on the current stream,
+        the export (kernel writing pinned host memory) on copy_stream."""
         from .device import CapturedSequence, _u64_to_i64
         slot = self.slots[self._next]
         self._next = (self._next + 1) % len(self.slots)
         st = torch.cuda.current_stream(self.dev)
+        us, cs = self.upload_stream, self.copy_stream
         if slot.uploaded is not None:
             slot.uploaded.synchronize()        # its pinned inputs are free to refill
         slot.in_params.numpy()[:] = np.array([pack_params(*p, norm_c) for p in params],
                                              dtype=np.float64).reshape(self.m, -1)
         sd = [_u64_to_i64(v) for v in np.atleast_1d(np.asarray(seeds, dtype=object))]
         slot.in_seeds.numpy()[:] = sd * self.m if len(sd) == 1 else sd
-        if slot.copied is not None:
-            st.wait_event(slot.copied)         # its device outputs have left
-        slot.env_dev.copy_(env_host, non_blocking=True)
-        slot.init_dev.copy_(init_host, non_blocking=True)
-        slot.batch.params.copy_(slot.in_params, non_blocking=True)
-        slot.batch.seeds.copy_(slot.in_seeds, non_blocking=True)
-        slot.uploaded = torch.cuda.Event()
-        slot.uploaded.record(st)
-        # device part as one CUDA graph per slot (built on its first call):
-        # landscape preparation, reset, the window launches and the unpack
         if slot.graph is None:
+            # first use: capture the device part (landscape preparation,
+            # reset, the window launches) as one graph on the current stream
+            slot.env_dev.copy_(env_host)
+            slot.init_dev.copy_(init_host)
+            slot.batch.params.copy_(slot.in_params)
+            slot.batch.seeds.copy_(slot.in_seeds)
             slot.graph = CapturedSequence(slot.device_part)
+        with torch.cuda.stream(us):
+            if slot.computed is not None:
+                us.wait_event(slot.computed)   # its previous run has read the inputs
+            slot.env_dev.copy_(env_host, non_blocking=True)
+            slot.init_dev.copy_(init_host, non_blocking=True)
+            slot.batch.params.copy_(slot.in_params, non_blocking=True)
+            slot.batch.seeds.copy_(slot.in_seeds, non_blocking=True)
+            slot.uploaded = torch.cuda.Event()
+            slot.uploaded.record(us)
+        st.wait_event(slot.uploaded)
+        if slot.copied is not None:
+            st.wait_event(slot.copied)         # its previous export has read the state
         slot.graph.replay()
-        computed = torch.cuda.Event()
-        computed.record(st)
-        cs = self.copy_stream
+        slot.computed = torch.cuda.Event()
+        slot.computed.record(st)
         with torch.cuda.stream(cs):
-            cs.wait_event(computed)
-            slot.out_b.copy_(slot.bu, non_blocking=True)
-            slot.out_d.copy_(slot.bd, non_blocking=True)
-            slot.out_acc.copy_(slot.batch.acc, non_blocking=True)
-            slot.out_cnt.copy_(slot.batch.counters[:, : max(self.steps, 1)], non_blocking=True)
-            slot.out_init.copy_(slot.batch._init_burning_dev, non_blocking=True)
+            cs.wait_event(slot.computed)
+            slot.export(cs)
             slot.copied = torch.cuda.Event()
             slot.copied.record(cs)
         return EnsembleTicket(slot, self.steps)

@@ -184,7 +184,7 @@ def _load_full_state(batch: FireBatch, state: FireState):
     burned[:h, :w] = state.burned
     bits = np.packbits(burned.reshape(ty, 32, tx, 32).transpose(0, 2, 1, 3), axis=-1,
                        bitorder="little").view(np.uint32).reshape(-1)
-    batch.planes[2].copy_(torch.from_numpy(bits.view(np.int32)))
+    batch.planes[2:4].copy_(torch.from_numpy(bits.view(np.int32)).expand(2, -1))
     acc = torch.from_numpy(np.asarray(state.accumulator, dtype=np.float32))
     batch.acc[0].copy_(acc)
     assert batch.planes.shape[1] == words

@@ -99,12 +99,12 @@ class RowShard:
     def boundary(self, which: str):
         """(burning, burned) words of the first/last owned tile row."""
         ty = self.part.ghost_top if which == "first" else self.rows_tiles - 1 - self.part.ghost_bottom
-        return self._rows(self.batch.q & 1, ty), self._rows(2, ty)
+        return self._rows(self.batch.q & 1, ty), self._rows(2 + (self.batch.q & 1), ty)
 
     def ghost(self, which: str):
         """(burning, burned) words of the top/bottom ghost tile row."""
         ty = 0 if which == "top" else self.rows_tiles - 1
-        return self._rows(self.batch.q & 1, ty), self._rows(2, ty)
+        return self._rows(self.batch.q & 1, ty), self._rows(2 + (self.batch.q & 1), ty)
 
     def mark_ghosts(self, stream=None):
         st = self.batch.struct()

@@ -5,6 +5,7 @@ Bar (BASELINE.json north_star): fire-state grids bit-exact; burn
 probabilities and parameter gradients within 1e-5 relative (fp32 path).
 """
 import math
+import os
 
 import numpy as np
 import pytest
@@ -621,6 +622,38 @@ def test_ensemble_runner_host_api_matches_device_batch():
     np.testing.assert_array_equal(out.series, b.series())
 
 
+def test_state_export_pinned_and_written_flags():
+    """fc_state_export into pinned host memory (device-mapped) and into
+    device tensors equals fc_state_unpack + the acc plane; with per-tile
+    written flags a reused destination is exact across runs whose fires
+    cover different tiles (stale tiles are rewritten, ragged edges kept)."""
+    n, m = 200, 2
+    env = S.make_environment(n, seed=8)
+    dl = F.DeviceLandscape.from_environment(env)
+    g = F.FireBatch((n, n), m, max_steps=80)
+    dest = [torch.zeros((m, n, n), dtype=dt, pin_memory=True)
+            for dt in (torch.uint8, torch.uint8, torch.float32)]
+    written = torch.zeros((m, g.grid.tiles_y, g.grid.tiles_x), dtype=torch.uint8, device="cuda")
+    init_a = S.center_ignition(n)
+    init_b = np.zeros((n, n), dtype=bool)
+    init_b[190:193, 5:8] = True                      # bottom-left edge tile row
+    for ph, steps, init in ((0.9, 80, init_a), (0.4, 15, init_b), (0.9, 30, init_a)):
+        g.set_params(np.array([F.pack_params(0.045, 0.131, 0.078, ph, 0.3)] * m))
+        g.set_seeds([3, 4])
+        g.reset(init)
+        g.run(dl, steps)
+        bu, bd = g.unpack()
+        g.export(*dest, written=written)
+        dev = [torch.empty_like(d, device="cuda") for d in dest]
+        g.export(*dev)
+        torch.cuda.synchronize()
+        want = (bu.cpu(), bd.cpu(), g.acc.cpu())
+        for x, y, z in zip(dest, dev, want):
+            assert torch.equal(x, z) and torch.equal(y.cpu(), z)
+    with pytest.raises(ValueError):
+        g.export(torch.zeros((m, n, n), dtype=torch.uint8), None, None)  # not pinned
+
+
 def test_ensemble_runner_pipelined_submits():
     """submit() tickets (depth-2 slot ring, copies overlapping the next
     call) return the same results as synchronous calls, per submission."""
@@ -746,3 +779,39 @@ def test_ordered_ensemble_lists_match_dense_sweep(rng):
                     attach_steps=range(1, steps + 1), threads=4)
         bu, bd = (x.bool().cpu().numpy() for x in a.unpack())
         assert np.array_equal(bu[4], res.burning) and np.array_equal(bd[4], res.burned)
+
+
+def test_c1_full_size_members_match_oracle():
+    """BASELINE config 1 at full size (16 members x 2048^2 x 500 steps,
+    K = 8 windows, ordered lists, persistent CTAs taking several tile groups
+    each): two runs are byte-identical and members 0 and 11 equal the CPU
+    oracle (states bit-exact, acc within RTOL_ACC).  At this size tiles of
+    one launch are processed after their neighbours' new states are written,
+    which the small cases above do not exercise."""
+    H, M, STEPS = 2048, 16, 500
+    env = S.make_environment(H, seed=1)
+    ph = S.ensemble_ph(M)
+    params = [(0.045, 0.131, 0.078, float(p), 0.3) for p in ph]
+    init = S.center_ignition(H)
+    b = F.FireBatch((H, H), M, max_steps=STEPS)
+    b.set_params(np.array([F.pack_params(*p) for p in params]))
+    b.set_seeds(list(range(M)))
+    dl = F.DeviceLandscape.from_environment(env)
+    runs = []
+    for _ in range(2):
+        b.reset(init)
+        b.run(dl, STEPS, window=8)
+        bu, bd = b.unpack()
+        runs.append((bu.cpu().numpy(), bd.cpu().numpy(), b.acc.cpu().numpy(), b.series()))
+    for x, y in zip(*runs):
+        assert np.array_equal(x, y)
+    bu, bd, acc, ser = runs[0]
+    arr = S.reference_landscape_arrays(env, O.slope_from_altitude)
+    for m in (0, 11):
+        p = P(params[m])
+        res = O.run(**arr, params=p, init=init, steps=STEPS, seed=m,
+                    threads=os.cpu_count() or 1, want_jac=False)
+        assert np.array_equal(bu[m].astype(bool), res.burning)
+        assert np.array_equal(bd[m].astype(bool), res.burned)
+        assert np.array_equal(ser[m], res.series)
+        np.testing.assert_allclose(acc[m], res.acc, rtol=RTOL_ACC, atol=0)
