@@ -815,3 +815,63 @@ def test_c1_full_size_members_match_oracle():
         assert np.array_equal(bd[m].astype(bool), res.burned)
         assert np.array_equal(ser[m], res.series)
         np.testing.assert_allclose(acc[m], res.acc, rtol=RTOL_ACC, atol=0)
+
+
+def _final(b):
+    bu, bd = b.unpack()
+    out = [bu, bd, b.acc.clone(), b.t_ign.clone(), torch.as_tensor(b.series())]
+    if b.jac is not None:
+        out.append(b.jac.clone())
+    return out
+
+
+def test_c3_full_size_window_and_sweep_invariance():
+    """BASELINE config 3 size (16384^2, 8 random 5x5 fires, sigma x32
+    landscape): one step per launch (no halo re-evolution), 8 and 16 fused
+    steps with activity lists, and 8 fused steps with the dense sweep give
+    byte-identical states, accumulators, ignition steps and series."""
+    n, steps = 16384, 240
+    e = S.make_environment_torch(n, n, seed=3)
+    dl = F.DeviceLandscape.from_elevation(e["elevation"], e["wind_speed"], e["wind_direction"],
+                                          e["canopy"], e["density"])
+    del e
+    init = torch.as_tensor(S.random_blocks(n, n, 8, 5, seed=3).astype(np.uint8), device="cuda")
+    b = F.FireBatch((n, n), 1, max_steps=steps)
+    b.set_params(F.pack_params(0.045, 0.131, 0.078, 0.58, 0.3))
+    b.set_seeds([3])
+    ref = None
+    for k, skip in ((1, True), (8, True), (16, True), (8, False)):
+        b.reset(init)
+        b.run(dl, steps, window=k, skip_inactive=skip)
+        got = _final(b)
+        if ref is None:
+            ref = got
+            assert int(got[0].sum()) > 0
+        else:
+            for x, y in zip(got, ref):
+                assert torch.equal(x, y), (k, skip)
+
+
+def test_c4_shape_window_invariance_with_schedule():
+    """Config-4 shape (1024^2, rotating/ramping device wind schedule, every
+    step attached) with 48 members: K = 1 and K = 8 launches give identical
+    states, accumulators, ignition steps, Jacobians and series."""
+    n, m, steps = 1024, 48, 200
+    env = S.make_environment(n, seed=4)
+    dl = F.DeviceLandscape.from_environment(env)
+    sched = F.wind_ramp_schedule(steps)
+    init = S.center_ignition(n)
+    b = F.FireBatch((n, n), m, max_steps=steps, with_jacobian=True)
+    ph = S.ensemble_ph(m)
+    b.set_params(np.array([F.pack_params(0.045, 0.131, 0.078, float(p), 0.3) for p in ph]))
+    b.set_seeds(list(range(100, 100 + m)))
+    ref = None
+    for k in (1, 8):
+        b.reset(init)
+        b.run(dl, steps, window=k, attach=[True] * steps, wind_schedule=sched)
+        got = _final(b)
+        if ref is None:
+            ref = got
+        else:
+            for x, y in zip(got, ref):
+                assert torch.equal(x, y), k
