@@ -125,8 +125,11 @@ class EnsembleRunner:
         self.slots = [_Slot(self, device) for _ in range(depth)]
         self.dev = self.slots[0].batch.device
         self.batch = self.slots[0].batch
+        # the kernels run on a high-priority stream; the export's short CTAs
+        # (low priority) fill SMs the step kernel leaves idle
+        self.compute_stream = torch.cuda.Stream(device=self.dev, priority=-5)
         self.upload_stream = torch.cuda.Stream(device=self.dev)
-        self.copy_stream = torch.cuda.Stream(device=self.dev)
+        self.copy_stream = torch.cuda.Stream(device=self.dev, priority=0)
         self._next = 0
         s0 = self.slots[0]
         self.h2d_bytes = s0.env_dev.numel() * 4 + s0.init_dev.numel() + self.m * (8 + 1) * 8
@@ -156,13 +159,15 @@ class EnsembleRunner:
         uint8/bool; params: per-member (c1, c2, a, p_h, p_continue).
 
         Streams: uploads on upload_stream (overlapping the previous call's
-        kernels), the device part (one CUDA graph) on the current stream,
+        kernels), the device part (one CUDA graph) on the high-priority
+        compute_stream (after the work the caller's current stream holds),
         the export (kernel writing pinned host memory) on copy_stream."""
         from .device import CapturedSequence, _u64_to_i64
         slot = self.slots[self._next]
         self._next = (self._next + 1) % len(self.slots)
-        st = torch.cuda.current_stream(self.dev)
-        us, cs = self.upload_stream, self.copy_stream
+        caller = torch.cuda.current_stream(self.dev)
+        st, us, cs = self.compute_stream, self.upload_stream, self.copy_stream
+        st.wait_stream(caller)                 # work the caller queued before this call
         if slot.uploaded is not None:
             slot.uploaded.synchronize()        # its pinned inputs are free to refill
         slot.in_params.numpy()[:] = np.array([pack_params(*p, norm_c) for p in params],
@@ -176,7 +181,9 @@ class EnsembleRunner:
             slot.init_dev.copy_(init_host)
             slot.batch.params.copy_(slot.in_params)
             slot.batch.seeds.copy_(slot.in_seeds)
-            slot.graph = CapturedSequence(slot.device_part)
+            with torch.cuda.stream(st):
+                st.wait_stream(caller)
+                slot.graph = CapturedSequence(slot.device_part)
         with torch.cuda.stream(us):
             if slot.computed is not None:
                 us.wait_event(slot.computed)   # its previous run has read the inputs
@@ -189,7 +196,8 @@ class EnsembleRunner:
         st.wait_event(slot.uploaded)
         if slot.copied is not None:
             st.wait_event(slot.copied)         # its previous export has read the state
-        slot.graph.replay()
+        with torch.cuda.stream(st):
+            slot.graph.replay()
         slot.computed = torch.cuda.Event()
         slot.computed.record(st)
         with torch.cuda.stream(cs):
