@@ -310,10 +310,10 @@ def run_ours(args):
     total_ms = allreduce_max(float(sum(ms)), dev)
     cu = world * MEMBERS * CELL_UPDATES_PER_MEMBER * args.steps
     value = cu / (total_ms / 1e3)
-    # reset (pack, cells, flags) + one list-widening check per run + per window
-    # launch the work-ordering pass (ensembles) and the window kernel
     nwin = (STEPS + WINDOW - 1) // WINDOW
-    launches_per_step = 3 + 1 + nwin * (2 if MEMBERS >= 4 else 1)
+    # reset (pack_init, init_cells, init_flags) + ensure_marking + one window
+    # kernel per launch (list ordering is off in the default build, FC_ORDER)
+    launches_per_step = 3 + 1 + nwin
 
     # final-state sanity (affected counts) for the log
     ser = batch.series()
