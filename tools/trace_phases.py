@@ -56,6 +56,15 @@ def main():
     torch.cuda.synchronize()
     print(f"{work} launch {target}: {1e3 * e0.elapsed_time(e1):.1f} us")
     tr = trace.cpu().numpy().astype(np.float64)
+    cta = tr[:, 15, 0, :4]
+    cta = cta[cta[:, 0] > 0]
+    if len(cta):
+        t0 = cta[:, 0].min()
+        ent, ext = (cta[:, 0] - t0) / 1e3, (cta[:, 1] - t0) / 1e3
+        print(f"CTAs {len(cta)}, listed tiles {int(cta[0, 3])}: entry spread {ent.max():.1f} us, "
+              f"exit p10/p50/p90/max {np.percentile(ext, 10):.1f}/{np.median(ext):.1f}/"
+              f"{np.percentile(ext, 90):.1f}/{ext.max():.1f} us, groups per CTA mean "
+              f"{cta[:, 2].mean():.2f} max {cta[:, 2].max():.0f}")
     act = tr[:, 0, 0, 0] != 0
     tr = tr[act]
     print("CTAs traced", int(act.sum()))
