@@ -40,6 +40,16 @@ def main():
     if os.environ.get("AB_GRAPH"):
         g = F.CapturedSequence(c1)
         print("c1 graph replay ms/run %.3f" % timeit(g.replay))
+    if os.environ.get("AB_EMPTY"):
+        # same launches with no fire anywhere: every CTA finds an empty list
+        # and exits, so this is the fixed per-launch cost of the run
+        zero = torch.zeros_like(init)
+
+        def c1_empty():
+            b.reset(zero)
+            b.run(dl, 500, window=window)
+        ge = F.CapturedSequence(c1_empty)
+        print("c1 no-fire graph replay ms/run %.3f" % timeit(ge.replay))
     n = 1024
     env2 = S.make_environment(n, seed=2)
     dl2 = F.DeviceLandscape.from_environment(env2)
