@@ -149,6 +149,15 @@ size_t fc_loss_workspace_bytes(const fc_grid* g, int32_t n_targets);
 int fc_state_init(const fc_grid* g, const fc_state* s, const uint8_t* init,
                   int64_t member_stride, int32_t t0, fc_stream_t stream);
 
+/* fc_state_init for a state previously initialised by fc_state_init whose
+ * acc and t_ign have been written only by this library since (fc_run,
+ * fc_inject, fc_state_reset): acc and t_ign are rewritten only in tiles that
+ * held fire since the last reset (tile_first set) or hold initial fire now;
+ * every other cell already has acc = 0, t_ign = FC_T_NEVER.  Same result as
+ * fc_state_init at a fraction of the memory traffic.  tile_first must be set. */
+int fc_state_reset(const fc_grid* g, const fc_state* s, const uint8_t* init,
+                   int64_t member_stride, int32_t t0, fc_stream_t stream);
+
 /* Unpack the current state to uint8 grids [M][H][W] (either may be NULL);
  * phase = number of fc_run launches since fc_state_init (selects the
  * burning buffer).  Mirrors FireState.burning / burned (model.py:158-160). */

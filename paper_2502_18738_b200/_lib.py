@@ -30,6 +30,7 @@ NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", 
 
 # Every symbol include/firecell.h declares (checked by the CPU test suite).
 EXPORTS = ("fc_grid_make", "fc_plane_words", "fc_loss_workspace_bytes", "fc_state_init",
+           "fc_state_reset",
            "fc_state_unpack", "fc_state_export", "fc_host_device_pointer", "fc_inject", "fc_run", "fc_mark_ghosts", "fc_activity_scan",
            "fc_contract", "fc_loss_grad",
            "fc_loss_dense", "fc_adamw", "fc_uniform_grid", "fc_epoch_seed", "fc_build_fields",
@@ -101,6 +102,7 @@ def lib():
             "fc_plane_words": (C.c_size_t, [G]),
             "fc_loss_workspace_bytes": (C.c_size_t, [G, i32]),
             "fc_state_init": (C.c_int, [G, ST, vp, i64, i32, vp]),
+            "fc_state_reset": (C.c_int, [G, ST, vp, i64, i32, vp]),
             "fc_state_unpack": (C.c_int, [G, ST, i32, vp, vp, vp]),
             "fc_state_export": (C.c_int, [G, ST, i32, vp, vp, vp, vp, vp]),
             "fc_host_device_pointer": (C.c_int, [vp, C.POINTER(vp)]),

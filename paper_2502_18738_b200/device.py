@@ -253,6 +253,7 @@ class FireBatch:
         self.list_count = torch.zeros((2 * (self.max_steps + 3) + 1,), dtype=torch.int32, device=dev)
         self.tile_fire = torch.zeros((ntiles,), dtype=torch.uint8, device=dev)
         self.tile_first = torch.full((ntiles,), L.T_NEVER, dtype=torch.int32, device=dev)
+        self._cells_clean = False  # acc / t_ign hold no library-written state yet
         self._mode = None  # sweep mode since reset (activity lists vs dense rescans)
         self.params = torch.zeros((self.m, L.NPARAM), dtype=torch.float64, device=dev)
         self.seeds = torch.zeros((self.m,), dtype=torch.int64, device=dev)
@@ -321,8 +322,13 @@ class FireBatch:
         self._init_burning_dev.copy_(cnt.expand(self.m) if m8.dim() == 2 else cnt)
         self._init_mask = m8.contiguous()
         st = self.struct()
-        L.check(L.lib().fc_state_init(C.byref(self.grid), C.byref(st), L.ptr(self._init_mask),
-                                      stride, int(t0), L.stream_ptr(stream)), "fc_state_init")
+        # after the first full initialisation only the tiles that held fire
+        # are rewritten (fc_state_reset); external writes to acc / t_ign
+        # must call mark_cells_dirty() first
+        fn = L.lib().fc_state_reset if self._cells_clean else L.lib().fc_state_init
+        L.check(fn(C.byref(self.grid), C.byref(st), L.ptr(self._init_mask), stride, int(t0),
+                   L.stream_ptr(stream)), "fc_state_init")
+        self._cells_clean = True
         self.t = int(t0)
         self.q = 0
         self._mode = None
@@ -395,6 +401,11 @@ class FireBatch:
         L.check(L.lib().fc_inject(C.byref(self.grid), C.byref(st), L.ptr(t), len(rows), self.t,
                                   self.q, L.stream_ptr(stream)), "fc_inject")
         self._inj = t
+
+    def mark_cells_dirty(self):
+        """Call after writing acc or t_ign directly: the next reset then
+        rewrites every cell instead of only the tiles that held fire."""
+        self._cells_clean = False
 
     def unpack(self, stream=None):
         """(burning, burned) uint8 tensors (M, H, W) at the current step."""

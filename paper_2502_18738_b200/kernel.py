@@ -187,6 +187,7 @@ def _load_full_state(batch: FireBatch, state: FireState):
     batch.planes[2:4].copy_(torch.from_numpy(bits.view(np.int32)).expand(2, -1))
     acc = torch.from_numpy(np.asarray(state.accumulator, dtype=np.float32))
     batch.acc[0].copy_(acc)
+    batch.mark_cells_dirty()
     assert batch.planes.shape[1] == words
 
 

@@ -875,3 +875,34 @@ def test_c4_shape_window_invariance_with_schedule():
         else:
             for x, y in zip(got, ref):
                 assert torch.equal(x, y), k
+
+
+@pytest.mark.parametrize("per_member", [False, True])
+def test_lazy_reset_equals_full_init(per_member):
+    """fc_state_reset (rewrites acc / t_ign only in tiles that held fire)
+    leaves exactly the state fc_state_init writes, after runs whose fires
+    covered other tiles; ragged grid, broadcast and per-member masks."""
+    h, w, m = 150, 230, 3
+    env = S.make_environment(h, w, seed=9)
+    dl = F.DeviceLandscape.from_environment(env)
+    rng = np.random.default_rng(5)
+    masks = [(rng.random((m, h, w)) < 0.002) if per_member else (rng.random((h, w)) < 0.002)
+             for _ in range(3)]
+    used = F.FireBatch((h, w), m, max_steps=60)
+    used.set_params(np.array([F.pack_params(0.045, 0.131, 0.078, 0.9, 0.5)] * m))
+    used.set_seeds([1, 2, 3])
+    for k, mask in enumerate(masks):
+        used.reset(mask)
+        fresh = F.FireBatch((h, w), m, max_steps=60)
+        fresh.reset(mask)
+        assert torch.equal(used.acc, fresh.acc) and torch.equal(used.t_ign, fresh.t_ign)
+        assert torch.equal(used.planes, fresh.planes)
+        assert torch.equal(used.tile_first, fresh.tile_first)
+        used.run(dl, 40 - 10 * k)
+    # an external write forces the next reset to rewrite every cell
+    used.acc.fill_(0.5)
+    used.mark_cells_dirty()
+    used.reset(masks[0])
+    fresh = F.FireBatch((h, w), m, max_steps=60)
+    fresh.reset(masks[0])
+    assert torch.equal(used.acc, fresh.acc) and torch.equal(used.t_ign, fresh.t_ign)
