@@ -311,9 +311,10 @@ def run_ours(args):
     cu = world * MEMBERS * CELL_UPDATES_PER_MEMBER * args.steps
     value = cu / (total_ms / 1e3)
     nwin = (STEPS + WINDOW - 1) // WINDOW
-    # reset (pack_init, init_cells, init_flags) + ensure_marking + one window
-    # kernel per launch (list ordering is off in the default build, FC_ORDER)
-    launches_per_step = 3 + 1 + nwin
+    # reset (pack_init + tile_init; a reused batch resets lazily without
+    # init_cells) + ensure_marking + one window kernel per launch (list
+    # ordering is off in the default build, FC_ORDER)
+    launches_per_step = 2 + 1 + nwin
 
     # final-state sanity (affected counts) for the log
     ser = batch.series()
