@@ -292,6 +292,15 @@ int fc_landscape_build(int32_t height, int32_t width, const void* elevation,
                        int32_t slope_sign, float* env, float* slope4, double* env64, float* dir32,
                        fc_stream_t stream);
 
+/* fc_landscape_build on at most max_ctas CTAs (0 = as many as the grid
+ * needs).  The e2e runner builds the next call's landscape with a few CTAs on
+ * a low-priority stream while the current call's step kernels hold the SMs. */
+int fc_landscape_build_ctas(int32_t height, int32_t width, const void* elevation,
+                            const void* wind_speed, const void* wind_direction,
+                            const void* canopy, const void* density, int32_t input_is_f64,
+                            double cell_side, int32_t slope_sign, float* env, float* slope4,
+                            double* env64, float* dir32, int32_t max_ctas, fc_stream_t stream);
+
 /* ---------------------------------------------------------- diagnostics --- */
 int fc_last_cuda_error(void);
 const char* fc_version(void);

@@ -34,7 +34,7 @@ EXPORTS = ("fc_grid_make", "fc_plane_words", "fc_loss_workspace_bytes", "fc_stat
            "fc_state_unpack", "fc_state_export", "fc_host_device_pointer", "fc_inject", "fc_run", "fc_mark_ghosts", "fc_activity_scan",
            "fc_contract", "fc_loss_grad",
            "fc_loss_dense", "fc_adamw", "fc_uniform_grid", "fc_epoch_seed", "fc_build_fields",
-           "fc_landscape_build",
+           "fc_landscape_build", "fc_landscape_build_ctas",
            "fc_last_cuda_error", "fc_version", "fc_debug_set_trace")
 
 
@@ -120,6 +120,8 @@ def lib():
             "fc_build_fields": (C.c_int, [G, LS, vp, vp, i32, vp]),
             "fc_landscape_build": (C.c_int, [i32, i32, vp, vp, vp, vp, vp, i32, dbl, i32, vp, vp,
                                              vp, vp, vp]),
+            "fc_landscape_build_ctas": (C.c_int, [i32, i32, vp, vp, vp, vp, vp, i32, dbl, i32, vp,
+                                                  vp, vp, vp, i32, vp]),
             "fc_last_cuda_error": (C.c_int, []),
             "fc_version": (C.c_char_p, []),
             "fc_debug_set_trace": (None, [vp]),

@@ -19,6 +19,7 @@ submissions.
 """
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 from typing import Optional, Sequence
 
@@ -53,6 +54,13 @@ class _Slot:
         g = self.batch.grid
         self.env_dev = torch.empty((5, r.h, r.w), dtype=torch.float32, device=dev)
         self.init_dev = torch.empty((r.h, r.w), dtype=torch.uint8, device=dev)
+        # the kernel-layout landscape of the slot, rebuilt in place each call
+        # (fc_landscape_build_ctas on the upload stream)
+        env = torch.zeros((r.h, r.w, 4), dtype=torch.float32, device=dev)
+        env64 = torch.zeros((r.h, r.w, 5), dtype=torch.float64, device=dev)
+        slope4 = torch.zeros((r.h, r.w, 4), dtype=torch.float32, device=dev)
+        dir32 = torch.zeros((r.h, r.w, 2), dtype=torch.float32, device=dev)
+        self.land = DeviceLandscape(env, env64, cell_side=r.cell_side, slope4=slope4, dir32=dir32)
         self.out_b = torch.zeros((r.m, r.h, r.w), dtype=torch.uint8, pin_memory=True)
         self.out_d = torch.zeros((r.m, r.h, r.w), dtype=torch.uint8, pin_memory=True)
         self.out_acc = torch.zeros((r.m, r.h, r.w), dtype=torch.float32, pin_memory=True)
@@ -68,13 +76,20 @@ class _Slot:
         self.graph = None
         self.runner = r
 
+    def build_landscape(self, stream, max_ctas: int):
+        """fc_landscape_build_ctas from the uploaded rasters into the slot's
+        landscape buffers (bit-identical to DeviceLandscape.from_elevation)."""
+        from . import _lib as L
+        e, land = self.env_dev, self.land
+        L.check(L.lib().fc_landscape_build_ctas(
+            self.runner.h, self.runner.w, *[L.ptr(e[i]) for i in range(5)], 0,
+            float(self.runner.cell_side), 1, L.ptr(land.env), L.ptr(land.slope4),
+            L.ptr(land.env64), L.ptr(land.dir32), int(max_ctas), L.stream_ptr(stream)),
+            "fc_landscape_build_ctas")
+
     def device_part(self):
-        r, e = self.runner, self.env_dev
-        land = DeviceLandscape.from_elevation(e[0], e[1], e[2], e[3], e[4],
-                                              cell_side=r.cell_side, device=self.batch.device)
-        self._land = land  # keeps the graph's landscape buffers referenced
         self.batch.reset(self.init_dev)
-        self.batch.run(land, r.steps, rng=r.rng)
+        self.batch.run(self.land, self.runner.steps, rng=self.runner.rng)
 
     def export(self, stream):
         """fc_state_export into the pinned result arrays + the counters."""
@@ -128,7 +143,11 @@ class EnsembleRunner:
         # the kernels run on a high-priority stream; the export's short CTAs
         # (low priority) fill SMs the step kernel leaves idle
         self.compute_stream = torch.cuda.Stream(device=self.dev, priority=-5)
-        self.upload_stream = torch.cuda.Stream(device=self.dev)
+        self.upload_stream = torch.cuda.Stream(device=self.dev, priority=0)
+        # CTAs of the landscape build (0 = the full grid): its fp64 slope
+        # arithmetic needs the whole GPU -- on 4 / 8 / 16 / 32 CTAs a c1 call
+        # took 13.3 / 8.0 / 5.8 / 4.9 ms against 3.6 ms with the full grid
+        self.landscape_ctas = int(os.environ.get("FC_LANDSCAPE_CTAS", 0))
         self.copy_stream = torch.cuda.Stream(device=self.dev, priority=0)
         self._next = 0
         s0 = self.slots[0]
@@ -158,9 +177,10 @@ class EnsembleRunner:
         direction, canopy, density), ideally pinned; init_host: (H, W)
         uint8/bool; params: per-member (c1, c2, a, p_h, p_continue).
 
-        Streams: uploads on upload_stream (overlapping the previous call's
-        kernels), the device part (one CUDA graph) on the high-priority
-        compute_stream (after the work the caller's current stream holds),
+        Streams: uploads and the landscape build on upload_stream,
+        overlapping the previous call's kernels; the device
+        part (one CUDA graph: reset and run) on the high-priority
+        compute_stream, after the work the caller's current stream holds;
         the export (kernel writing pinned host memory) on copy_stream."""
         from .device import CapturedSequence, _u64_to_i64
         slot = self.slots[self._next]
@@ -181,6 +201,7 @@ class EnsembleRunner:
             slot.init_dev.copy_(init_host)
             slot.batch.params.copy_(slot.in_params)
             slot.batch.seeds.copy_(slot.in_seeds)
+            slot.build_landscape(caller, 0)
             with torch.cuda.stream(st):
                 st.wait_stream(caller)
                 slot.graph = CapturedSequence(slot.device_part)
@@ -191,6 +212,9 @@ class EnsembleRunner:
             slot.init_dev.copy_(init_host, non_blocking=True)
             slot.batch.params.copy_(slot.in_params, non_blocking=True)
             slot.batch.seeds.copy_(slot.in_seeds, non_blocking=True)
+            # the landscape of this call, built next to the previous call's
+            # step kernels
+            slot.build_landscape(us, self.landscape_ctas)
             slot.uploaded = torch.cuda.Event()
             slot.uploaded.record(us)
         st.wait_event(slot.uploaded)
