@@ -380,7 +380,8 @@ def run_ours(args):
            "h2d_bytes_per_step": int(runner.h2d_bytes), "d2h_bytes_per_step": int(runner.d2h_bytes(prev)),
            "d2h_note": "fc_state_export writes the (M,H,W) burning/burned/accumulator result "
                        "arrays in pinned host memory from the device, only for tiles affected "
-                       "now or written by the slot's previous call (%d of %d tiles); the "
+                       "now or written by the slot's previous call (%d of %d tiles, in 128-column "
+                       "spans); the "
                        "dense arrays would be %d B" % (prev.exported_tiles(),
                                                        runner.batch.grid.tiles_x * runner.batch.grid.tiles_y * MEMBERS,
                                                        runner.d2h_bytes_dense),

@@ -157,19 +157,22 @@ class EnsembleRunner:
                                 + self.m * self.steps * 4 * 4)
 
     def d2h_bytes(self, ticket: EnsembleTicket) -> int:
-        """Bytes one call moved device -> host: the exported tiles (1 + 1 + 4
-        B per cell) and the counters."""
+        """Bytes one call moved device -> host (after result(); syncs): the
+        export writes whole 128-column spans (4 tiles) that hold a written
+        tile, 1 + 1 + 4 B per cell, plus the per-step counters.  Counted from
+        the slot's written flags, i.e. exact when consecutive calls affect the
+        same tiles (the bench repeats one workload)."""
         g = ticket.slot.batch.grid
-        full_tiles = (self.h // 32) * (self.w // 32) == g.tiles_y * g.tiles_x
-        per_tile = 32 * 32 * 6 if full_tiles else None
-        n = ticket.exported_tiles()
-        if per_tile is None:  # ragged edges: count cells of the written tiles exactly
-            w = ticket.slot.written.to(torch.int64).cpu().numpy()
-            rows = np.minimum(32, self.h - 32 * np.arange(g.tiles_y))[:, None]
-            cols = np.minimum(32, self.w - 32 * np.arange(g.tiles_x))[None, :]
-            cells = int((w * (rows * cols)[None]).sum())
-            return cells * 6 + self.m * (self.steps * 16 + 8)
-        return n * per_tile + self.m * (self.steps * 16 + 8)
+        w = ticket.slot.written.to(torch.bool).cpu().numpy()          # (M, TY, TX)
+        span = 4
+        nsp = (g.tiles_x + span - 1) // span
+        pad = np.zeros((w.shape[0], w.shape[1], nsp * span), dtype=bool)
+        pad[:, :, : g.tiles_x] = w
+        dirty = pad.reshape(w.shape[0], w.shape[1], nsp, span).any(-1)  # (M, TY, nsp)
+        rows = np.minimum(32, self.h - 32 * np.arange(g.tiles_y))[:, None]
+        cols = np.minimum(128, self.w - 128 * np.arange(nsp))[None, :]
+        cells = int((dirty * (rows * cols)[None]).sum())
+        return cells * 6 + self.m * (self.steps * 16 + 8)
 
     def submit(self, env_host: torch.Tensor, init_host: torch.Tensor, params: Sequence,
                seeds: Sequence[int], norm_c: float = DEFAULT_NORM_C) -> EnsembleTicket:
