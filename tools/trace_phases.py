@@ -65,6 +65,22 @@ def main():
               f"exit p10/p50/p90/max {np.percentile(ext, 10):.1f}/{np.median(ext):.1f}/"
               f"{np.percentile(ext, 90):.1f}/{ext.max():.1f} us, groups per CTA mean "
               f"{cta[:, 2].mean():.2f} max {cta[:, 2].max():.0f}")
+    if len(cta) and os.environ.get("TRACE_CORR"):
+        # per CTA: chain (entry -> exit), summed per-step item rounds and
+        # item-phase critical cycles; which one explains the slowest CTAs?
+        full = trace.cpu().numpy().astype(np.float64)
+        ok = full[:, 15, 0, 0] > 0
+        ch = (full[ok, 15, 0, 1] - full[ok, 15, 0, 0]) / 1e3
+        rounds = full[ok, :8, :, 3].max(axis=2).sum(axis=1)
+        crit = (full[ok, :8, :, 2].max(axis=2) - full[ok, :8, :, 1].min(axis=2)).clip(0).sum(axis=1)
+        swp = (full[ok, :8, :, 1].min(axis=2) - full[ok, :8, :, 0].min(axis=2)).clip(0).sum(axis=1)
+        print(f"corr(chain, rounds) {np.corrcoef(ch, rounds)[0, 1]:.2f}  corr(chain, item crit) "
+              f"{np.corrcoef(ch, crit)[0, 1]:.2f}  corr(chain, sweep) {np.corrcoef(ch, swp)[0, 1]:.2f}")
+        order = np.argsort(ch)
+        for lab, idx in (("fastest", order[:5]), ("slowest", order[-5:])):
+            for i in idx:
+                print(f"  {lab} chain {ch[i]:6.1f} us rounds {rounds[i]:4.0f} item-crit {crit[i]:7.0f} "
+                      f"sweep {swp[i]:6.0f} cycles")
     act = tr[:, 0, 0, 0] != 0
     tr = tr[act]
     print("CTAs traced", int(act.sum()))
