@@ -251,7 +251,8 @@ class EnsembleCalibrator:
     def __init__(self, land: DeviceLandscape, init, targets: torch.Tensor,
                  obs_steps: Sequence[int], members: Sequence[int], params, *,
                  steps: Optional[int] = None, wind_schedule: Optional[torch.Tensor] = None,
-                 lr: float = 1e-2, weight_decay: float = 0.0, window: int = 8, device=None):
+                 lr: float = 1e-2, weight_decay: float = 0.0, window: Optional[int] = None,
+                 device=None):
         from .parallel import allreduce_sum_  # noqa: F401  (import check)
         self.land, self.lr, self.wd, self.window = land, lr, weight_decay, window
         self.steps = int(steps if steps is not None else max(obs_steps))
