@@ -81,11 +81,12 @@ class _Slot:
         landscape buffers (bit-identical to DeviceLandscape.from_elevation)."""
         from . import _lib as L
         e, land = self.env_dev, self.land
-        L.check(L.lib().fc_landscape_build_ctas(
-            self.runner.h, self.runner.w, *[L.ptr(e[i]) for i in range(5)], 0,
-            float(self.runner.cell_side), 1, L.ptr(land.env), L.ptr(land.slope4),
-            L.ptr(land.env64), L.ptr(land.dir32), int(max_ctas), L.stream_ptr(stream)),
-            "fc_landscape_build_ctas")
+        with torch.cuda.device(self.batch.device):  # the launch goes to this device
+            L.check(L.lib().fc_landscape_build_ctas(
+                self.runner.h, self.runner.w, *[L.ptr(e[i]) for i in range(5)], 0,
+                float(self.runner.cell_side), 1, L.ptr(land.env), L.ptr(land.slope4),
+                L.ptr(land.env64), L.ptr(land.dir32), int(max_ctas), L.stream_ptr(stream)),
+                "fc_landscape_build_ctas")
 
     def device_part(self):
         self.batch.reset(self.init_dev)
@@ -97,9 +98,10 @@ class _Slot:
         from . import _lib as L
         b = self.batch
         st = b.struct()
-        L.check(L.lib().fc_state_export(C.byref(b.grid), C.byref(st), b.q, *self.out_ptrs,
-                                        L.ptr(self.written), L.stream_ptr(stream)),
-                "fc_state_export")
+        with torch.cuda.device(b.device):
+            L.check(L.lib().fc_state_export(C.byref(b.grid), C.byref(st), b.q, *self.out_ptrs,
+                                            L.ptr(self.written), L.stream_ptr(stream)),
+                    "fc_state_export")
         self.out_cnt.copy_(b.counters[:, : max(self.runner.steps, 1)], non_blocking=True)
         self.out_init.copy_(b._init_burning_dev, non_blocking=True)
 
