@@ -906,3 +906,35 @@ def test_lazy_reset_equals_full_init(per_member):
     fresh = F.FireBatch((h, w), m, max_steps=60)
     fresh.reset(masks[0])
     assert torch.equal(used.acc, fresh.acc) and torch.equal(used.t_ign, fresh.t_ign)
+
+
+def test_no_fire_run_and_export():
+    """An empty initial mask: every launch finds an empty activity list; the
+    state, accumulator, series and export stay zero, for list and dense
+    sweeps, and a later reset with fire runs normally (equals a fresh batch)."""
+    h, w, m = 100, 130, 2
+    env = S.make_environment(h, w, seed=3)
+    dl = F.DeviceLandscape.from_environment(env)
+    for skip in (True, False):
+        b = F.FireBatch((h, w), m, max_steps=40)
+        b.set_params(np.array([F.pack_params(0.045, 0.131, 0.078, 0.9, 0.5)] * m))
+        b.set_seeds([1, 2])
+        b.reset(np.zeros((h, w), dtype=bool))
+        b.run(dl, 20, skip_inactive=skip)
+        bu, bd = b.unpack()
+        assert not bu.any() and not bd.any() and not b.acc.any()
+        assert not np.asarray(b.series()).any()
+        dest = [torch.zeros((m, h, w), dtype=dt, pin_memory=True)
+                for dt in (torch.uint8, torch.uint8, torch.float32)]
+        b.export(*dest)
+        torch.cuda.synchronize()
+        assert not any(bool(x.any()) for x in dest)
+        b.reset(S.center_ignition(h, w))
+        b.run(dl, 20, skip_inactive=skip)
+        f = F.FireBatch((h, w), m, max_steps=40)
+        f.set_params(np.array([F.pack_params(0.045, 0.131, 0.078, 0.9, 0.5)] * m))
+        f.set_seeds([1, 2])
+        f.reset(S.center_ignition(h, w))
+        f.run(dl, 20, skip_inactive=skip)
+        for x, y in zip(_final(b), _final(f)):
+            assert torch.equal(x, y)
