@@ -280,7 +280,7 @@ def run_ours(args):
     ph_all = S.ensemble_ph(MEMBERS * world)
     params = [(0.045, 0.131, 0.078, float(ph_all[m]), 0.3) for m in members]
     init = S.center_ignition(H)
-    batch = F.FireBatch((H, W), MEMBERS, max_steps=STEPS, device=dev)
+    batch = F.FireBatch((H, W), MEMBERS, max_steps=STEPS, member0=members[0], device=dev)
     batch.set_params(np.array([F.pack_params(*p) for p in params]))
     batch.set_seeds(members)
     init_dev = torch.as_tensor(init.astype(np.uint8), device=dev)

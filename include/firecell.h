@@ -124,15 +124,18 @@ typedef struct {
     int32_t pad_;
 } fc_state;
 
-/* Row-sharded single domain (BASELINE config 3 across GPUs): the local grid
- * holds this rank's rows plus ghost tile rows (32 rows each) copied from the
- * neighbouring ranks after every launch.  Ghost tiles are read as halo and
- * never advanced; draws are keyed by the global row = local row + row0. */
+/* Position of this state in a partitioned job.  Row-sharded single domain
+ * (BASELINE config 3 across GPUs): the local grid holds this rank's rows plus
+ * ghost tile rows (32 rows each) copied from the neighbouring ranks after
+ * every launch.  Ghost tiles are read as halo and never advanced; draws are
+ * keyed by the global row = local row + row0.  Member-sharded ensembles
+ * (configs 1 and 4): local member m is global member m + member0, the member
+ * word of the Philox counter, so a member draws the same numbers on any rank. */
 typedef struct {
     int32_t row0;           /* global row of local row 0                    */
     int32_t ghost_top;      /* ghost tile rows at the top (0 or 1)          */
     int32_t ghost_bottom;   /* ghost tile rows at the bottom (0 or 1)       */
-    int32_t pad_;
+    int32_t member0;        /* global index of local member 0               */
 } fc_shard;
 
 /* ------------------------------------------------------------ sizing --- */
@@ -204,7 +207,8 @@ int fc_inject(const fc_grid* g, const fc_state* s, const int32_t* cells, int32_t
  * indexed by pre-step index: step t sees speed alpha*V + beta and direction
  * theta + gamma (a WindUpdate, kernel.py:422-428/505-511, for every step
  * without re-uploading fields; config 4's rotating, ramping wind).
- * shard: NULL, or the row-shard descriptor (ghost rows are not advanced).
+ * shard: NULL, or the partition descriptor (global row / member offsets;
+ * ghost rows are not advanced).
  * host_phase: in/out launch counter (see fc_state_unpack). */
 int fc_run(const fc_grid* g, const fc_landscape* land, const fc_state* s,
            const double* params, const uint64_t* seeds, int32_t rng_mode,

@@ -113,6 +113,12 @@ typedef struct {
     double c1, c2, a, p_h, p_continue, norm_c;
     int factor_source;     /* 0 = "target" (default), 1 = "source"   */
     int slope_radians;     /* slope_units == "radians"               */
+    int64_t row0, col0;    /* absolute position of local cell (0, 0): draws are keyed
+                              by the absolute cell (rng.py:64-67), so a crop of a
+                              larger domain sees the domain's draws               */
+    const double* wsched;  /* NULL, or [steps][4] per pre-step index t: the wind of
+                              step t is a WindUpdate (kernel.py:422-428) with fields
+                              alpha*V + beta and theta + gamma (base fields vw/wdir) */
 } orc_model;
 
 /* One slot's cached quantities, restating build_fields (kernel.py:165-195)
@@ -120,12 +126,17 @@ typedef struct {
 typedef struct { double fp, raw, rest, vw, cosm1, slope; } orc_slot;
 
 static inline void orc_slot_eval(const orc_model* m, const double* vw, const double* wdir,
-                                 int sr, int sc, int tr, int tc, int k, orc_slot* o) {
+                                 const double* ws, int sr, int sc, int tr, int tc, int k,
+                                 orc_slot* o) {
     const int w = m->w;
     size_t src = (size_t)sr * w + sc, tgt = (size_t)tr * w + tc;
     int dr = -ORC_POS[k][0], dc = -ORC_POS[k][1];
-    double v = vw[src];
-    double cosm1 = cos((wdir[src] - ORC_BEAR[k]) * (3.141592653589793 / 180.0)) - 1.0;
+    double v = vw[src], th = wdir[src];
+    if (ws) {  /* the WindUpdate's fields, computed elementwise in fp64 */
+        v = ws[0] * v + ws[1];
+        th = th + ws[2];
+    }
+    double cosm1 = cos((th - ORC_BEAR[k]) * (3.141592653589793 / 180.0)) - 1.0;
     double s = m->slope9[src * 9 + (1 + dr) * 3 + (1 + dc)];
     if (m->slope_radians) s = s * (180.0 / 3.141592653589793);
     size_t site = m->factor_source ? src : tgt;
@@ -135,6 +146,39 @@ static inline void orc_slot_eval(const orc_model* m, const double* vw, const dou
     double raw = m->p_h * rest;                                        /* kernel.py:189 */
     o->fp = tanh(m->norm_c * raw);                                     /* kernel.py:190 */
     o->raw = raw; o->rest = rest; o->vw = v; o->cosm1 = cosm1; o->slope = s;
+}
+
+/* Conditioning of J for an fp32 evaluation of the same formulas (test
+ * infrastructure: the scale against which an fp32 J is judged).  A slot's
+ * exponent c1 V + c2 V (cos - 1) + a S carries an absolute error of about
+ * E 2^-23 with E = |c1 V| + |c2| (|V (cos - 1)| + 4 |V|) + |a S| (fp32
+ * operands; the wind term is formed from an fp32 wind vector), so its factor
+ * 1 - fp has relative error r = 2^-23 (E + 2) (1 + 2y) once y = c raw
+ * saturates (1 - tanh y ~ 2 e^-2y amplifies the error of y by 2y).  Each
+ * term of J is a product over the live slots' factors: its bound is the term
+ * times the sum of r; the c2 term adds the absolute error of cos - 1 formed
+ * from the fp32 wind vector, 2^-21 |chain raw V|. */
+static void orc_fp32_cond(const orc_model* m, const orc_slot* sl, const int* live,
+                          const double* pre, const double* suf, double* out) {
+    double R = 0.0;
+    for (int k = 0; k < 8; ++k) {
+        if (!live[k]) continue;
+        const double v = fabs(sl[k].vw);
+        const double E = fabs(m->c1) * v + fabs(m->c2) * (v * fabs(sl[k].cosm1) + 4.0 * v) +
+                         fabs(m->a * sl[k].slope);
+        const double y = m->norm_c * sl[k].raw;
+        R += 0x1p-23 * (E + 2.0) * (1.0 + (y > 0.55 ? 2.0 * y : 0.0));
+    }
+    double o0 = 0, o1 = 0, o2 = 0, o3 = 0;
+    for (int k = 0; k < 8; ++k) {
+        if (!live[k]) continue;
+        const double ch = fabs(pre[k] * suf[k] * (m->norm_c * (1.0 - sl[k].fp * sl[k].fp)));
+        o0 += ch * fabs(sl[k].raw * sl[k].vw) * R;
+        o1 += ch * fabs(sl[k].raw * sl[k].vw) * (fabs(sl[k].cosm1) * R + 0x1p-21);
+        o2 += ch * fabs(sl[k].raw * sl[k].slope) * R;
+        o3 += ch * fabs(sl[k].rest) * R;
+    }
+    out[0] = o0; out[1] = o1; out[2] = o2; out[3] = o3;
 }
 
 /* Precomputed per-slot normalized probabilities, fp[k][i] at source cell i
@@ -149,7 +193,7 @@ static void orc_build_fp(const orc_model* m, const double* vw, const double* wdi
                 double val = 0.0;
                 if (tr >= 0 && tr < h && tc >= 0 && tc < w) {
                     orc_slot s;
-                    orc_slot_eval(m, vw, wdir, r, c, tr, tc, k, &s);
+                    orc_slot_eval(m, vw, wdir, NULL, r, c, tr, tc, k, &s);
                     val = s.fp;
                 } else {
                     /* target outside the grid: the reference still fills the
@@ -173,6 +217,13 @@ static void orc_build_fp(const orc_model* m, const double* vw, const double* wdi
  * attach: array of steps+1 flags, attach[s] for 1-based step s.
  * Outputs: burning/burned (uint8), acc (fp64), t_ign (int32: pre-step index
  * of ignition, -1 initial, INT32_MAX never), jac (h*w*4 fp64, may be NULL),
+ * jac_abs (h*w*4: the sum of the absolute slot terms of each J component --
+ * the scale against which a rounded J is judged; may be NULL), jac_floor
+ * (h*w*4: the absolute rounding floor of the reference's own J -- where a
+ * slot saturates, fp is within ulps of 1 and the factors 1 - fp and 1 - fp^2
+ * of tape.py:106-147 cancel; each term recomputed with those factors
+ * inflated by their fp64 error, minus the term; may be NULL), jac_cond
+ * (h*w*4: the fp32 conditioning of J -- see orc_fp32_cond; may be NULL),
  * series (steps*2 int64: burning, burned after each step),
  * n_entries (tape entries = ignitions on attached steps).
  */
@@ -180,7 +231,8 @@ int orc_run(const orc_model* m, const uint8_t* init, int steps, uint64_t seed,
             int n_wind, const int* wind_at, const double* wind_v, const double* wind_d,
             const uint8_t* attach, int threads,
             uint8_t* burning, uint8_t* burned, double* acc, int32_t* t_ign,
-            double* jac, int64_t* series, int64_t* n_entries) {
+            double* jac, double* jac_abs, double* jac_floor, double* jac_cond,
+            int64_t* series, int64_t* n_entries) {
     const int h = m->h, w = m->w;
     const size_t n = (size_t)h * w;
 #ifdef _OPENMP
@@ -199,6 +251,9 @@ int orc_run(const orc_model* m, const uint8_t* init, int steps, uint64_t seed,
         nburning += burning[i];
     }
     if (jac) memset(jac, 0, sizeof(double) * n * 4);
+    if (jac_abs) memset(jac_abs, 0, sizeof(double) * n * 4);
+    if (jac_floor) memset(jac_floor, 0, sizeof(double) * n * 4);
+    if (jac_cond) memset(jac_cond, 0, sizeof(double) * n * 4);
     int64_t nburned = 0, entries = 0;
 
     double* fp = (double*)malloc(sizeof(double) * n * 8);
@@ -206,17 +261,20 @@ int orc_run(const orc_model* m, const uint8_t* init, int steps, uint64_t seed,
     if (!fp || !prev) { free(fp); free(prev); return -2; }
     const double* vw = m->vw;
     const double* wdir = m->wdir;
-    orc_build_fp(m, vw, wdir, fp);
+    if (!m->wsched) orc_build_fp(m, vw, wdir, fp);
     int next_wind = 0;
 
     for (int s = 1; s <= steps; ++s) {
         while (next_wind < n_wind && wind_at[next_wind] == s) {   /* kernel.py:505-511 */
             vw = wind_v + (size_t)next_wind * n;
             wdir = wind_d + (size_t)next_wind * n;
-            orc_build_fp(m, vw, wdir, fp);
+            if (!m->wsched) orc_build_fp(m, vw, wdir, fp);
             ++next_wind;
         }
         const uint64_t t = (uint64_t)(s - 1);  /* pre-step index, kernel.py:295 */
+        /* parametric schedule: the step's fields are evaluated per live slot
+         * (the same values build_fields would tabulate for this step) */
+        const double* ws = m->wsched ? m->wsched + (size_t)t * 4 : NULL;
         int do_attach = attach ? attach[s] : 0;
         /* _burning_bbox, kernel.py:208-213, + 1-cell margin kernel.py:301-302 */
         int rmin = h, rmax = -1, cmin = w, cmax = -1;
@@ -247,7 +305,8 @@ int orc_run(const orc_model* m, const uint8_t* init, int steps, uint64_t seed,
                     size_t j = (size_t)r * w + c;
                     if (prev[j]) {
                         /* keeps = burning & (u_C < p_continue), kernel.py:248-253 */
-                        double u = orc_cell_draw(key_c, (uint64_t)r, (uint64_t)c);
+                        double u = orc_cell_draw(key_c, (uint64_t)(r + m->row0),
+                                                 (uint64_t)(c + m->col0));
                         if (!(u < m->p_continue)) {
                             burning[j] = 0;
                             burned[j] = 1;
@@ -264,12 +323,20 @@ int orc_run(const orc_model* m, const uint8_t* init, int steps, uint64_t seed,
                         if (sr < 0 || sr >= h || sc < 0 || sc >= w) continue;
                         size_t i = (size_t)sr * w + sc;
                         if (!prev[i]) continue;
-                        prod *= 1.0 - fp[(size_t)k * n + i];
+                        double f;
+                        if (ws) {
+                            orc_slot sk;
+                            orc_slot_eval(m, vw, wdir, ws, sr, sc, r, c, k, &sk);
+                            f = sk.fp;
+                        } else {
+                            f = fp[(size_t)k * n + i];
+                        }
+                        prod *= 1.0 - f;
                         any = 1;
                     }
                     if (!any) continue;
                     double p = 1.0 - prod;
-                    double u = orc_cell_draw(key_i, (uint64_t)r, (uint64_t)c);
+                    double u = orc_cell_draw(key_i, (uint64_t)(r + m->row0), (uint64_t)(c + m->col0));
                     if (!(u < p)) continue;  /* kernel.py:246-247 strict < */
                     burning[j] = 1;
                     acc[j] = p;              /* kernel.py:254-255 */
@@ -285,7 +352,7 @@ int orc_run(const orc_model* m, const uint8_t* init, int steps, uint64_t seed,
                             live[k] = (sr >= 0 && sr < h && sc >= 0 && sc < w &&
                                        prev[(size_t)sr * w + sc]);
                             if (live[k]) {
-                                orc_slot_eval(m, vw, wdir, sr, sc, r, c, k, &sl[k]);
+                                orc_slot_eval(m, vw, wdir, ws, sr, sc, r, c, k, &sl[k]);
                                 fac[k] = 1.0 - sl[k].fp;
                             } else {
                                 fac[k] = 1.0;
@@ -299,14 +366,45 @@ int orc_run(const orc_model* m, const uint8_t* init, int steps, uint64_t seed,
                             suf[7 - k] = suf[8 - k] * fac[8 - k];
                         }
                         double g0 = 0, g1 = 0, g2 = 0, g3 = 0;
+                        double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+                        double f0 = 0, f1 = 0, f2 = 0, f3 = 0;
+                        /* rounding floor: every factor that cancels near a
+                         * saturated slot (1 - fp, 1 - fp^2 with fp within ulps
+                         * of 1) inflated by its fp64 absolute error (a tanh
+                         * within 2 ulps on either side: 2^-50, and 2^-49 for
+                         * the square) -- an interval bound on |J - J_exact| */
+                        double hp[8], hs[8];
+                        hp[0] = 1.0;
+                        hs[7] = 1.0;
+                        for (int k = 1; k < 8; ++k) {
+                            hp[k] = hp[k - 1] * (live[k - 1] ? fac[k - 1] + 0x1p-50 : 1.0);
+                            hs[7 - k] = hs[8 - k] * (live[8 - k] ? fac[8 - k] + 0x1p-50 : 1.0);
+                        }
                         for (int k = 0; k < 8; ++k) {
                             if (!live[k]) continue;
                             double ch = pre[k] * suf[k] * (m->norm_c * (1.0 - sl[k].fp * sl[k].fp));
-                            g0 += ch * sl[k].raw * sl[k].vw;
-                            g1 += ch * sl[k].raw * sl[k].vw * sl[k].cosm1;
-                            g2 += ch * sl[k].raw * sl[k].slope;
-                            g3 += ch * sl[k].rest;
+                            double t0_ = ch * sl[k].raw * sl[k].vw;
+                            double t1_ = ch * sl[k].raw * sl[k].vw * sl[k].cosm1;
+                            double t2_ = ch * sl[k].raw * sl[k].slope;
+                            double t3_ = ch * sl[k].rest;
+                            g0 += t0_; g1 += t1_; g2 += t2_; g3 += t3_;
+                            a0 += fabs(t0_); a1 += fabs(t1_); a2 += fabs(t2_); a3 += fabs(t3_);
+                            double chh = hp[k] * hs[k] *
+                                         (m->norm_c * (fabs(1.0 - sl[k].fp * sl[k].fp) + 0x1p-49));
+                            f0 += fabs(chh * sl[k].raw * sl[k].vw) - fabs(t0_);
+                            f1 += fabs(chh * sl[k].raw * sl[k].vw * sl[k].cosm1) - fabs(t1_);
+                            f2 += fabs(chh * sl[k].raw * sl[k].slope) - fabs(t2_);
+                            f3 += fabs(chh * sl[k].rest) - fabs(t3_);
                         }
+                        if (jac_abs) {
+                            jac_abs[j * 4 + 0] = a0; jac_abs[j * 4 + 1] = a1;
+                            jac_abs[j * 4 + 2] = a2; jac_abs[j * 4 + 3] = a3;
+                        }
+                        if (jac_floor) {
+                            jac_floor[j * 4 + 0] = f0; jac_floor[j * 4 + 1] = f1;
+                            jac_floor[j * 4 + 2] = f2; jac_floor[j * 4 + 3] = f3;
+                        }
+                        if (jac_cond) orc_fp32_cond(m, sl, live, pre, suf, jac_cond + j * 4);
                         jac[j * 4 + 0] = g0;
                         jac[j * 4 + 1] = g1;
                         jac[j * 4 + 2] = g2;

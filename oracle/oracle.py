@@ -58,7 +58,7 @@ def lib():
         L.orc_run.argtypes = [C.c_void_p, C.c_void_p, C.c_int, u64, C.c_int, C.c_void_p,
                               C.c_void_p, C.c_void_p, C.c_void_p, C.c_int,
                               C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
-                              C.c_void_p, C.c_void_p]
+                              C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.orc_combined_loss.restype = C.c_int
         L.orc_combined_loss.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int,
                                         C.c_void_p, C.c_void_p, C.c_void_p]
@@ -110,7 +110,8 @@ class _Model(C.Structure):
                 ("canopy", C.c_void_p), ("density", C.c_void_p),
                 ("c1", C.c_double), ("c2", C.c_double), ("a", C.c_double),
                 ("p_h", C.c_double), ("p_continue", C.c_double), ("norm_c", C.c_double),
-                ("factor_source", C.c_int), ("slope_radians", C.c_int)]
+                ("factor_source", C.c_int), ("slope_radians", C.c_int),
+                ("row0", C.c_int64), ("col0", C.c_int64), ("wsched", C.c_void_p)]
 
 
 @dataclass
@@ -122,6 +123,9 @@ class OracleResult:
     jac: Optional[np.ndarray]
     series: np.ndarray       # (steps, 2): burning, burned after each step
     n_entries: int
+    jac_abs: Optional[np.ndarray] = None    # sum of |slot terms| per J component
+    jac_floor: Optional[np.ndarray] = None  # rounding floor of the reference's own J
+    jac_cond: Optional[np.ndarray] = None   # conditioning of an fp32 evaluation of J
 
     def affected(self):
         return self.burning | self.burned
@@ -129,11 +133,17 @@ class OracleResult:
 
 def run(wind_speed, wind_direction, slope, canopy, density, params, init, steps, seed, *,
         attach_steps=(), wind_schedule=(), norm_c=DEFAULT_NORM_C, factor_site="target",
-        slope_units="degrees", threads=1, want_jac=None) -> OracleResult:
+        slope_units="degrees", threads=1, want_jac=None, origin=(0, 0), wind_params=None,
+        want_jac_abs=False) -> OracleResult:
     """Restates run_simulation (kernel.py:453-529).
 
     params: object with c1, c2, a, p_h, p_continue (floats).
     wind_schedule: iterable of (apply_at_step, speed, direction).
+    origin: absolute (row, col) of local cell (0, 0) -- the arrays are a crop
+    of a larger domain, draws keyed by the absolute cell (rng.py:64-67).
+    wind_params: optional (steps, >=3) rows (alpha, beta, gamma_deg) per
+    pre-step index: step t runs on the WindUpdate fields alpha*V + beta,
+    theta + gamma of the base fields (the parametric form of kernel.py:505-511).
     """
     f64 = lambda x: np.ascontiguousarray(x, dtype=np.float64)
     vw, wd, sl, ca, de = f64(wind_speed), f64(wind_direction), f64(slope), f64(canopy), f64(density)
@@ -150,25 +160,35 @@ def run(wind_speed, wind_direction, slope, canopy, density, params, init, steps,
             attach[int(s)] = 1
     if want_jac is None:
         want_jac = bool(attach.any())
+    wp = None
+    if wind_params is not None:
+        wp = np.zeros((max(steps, 1), 4), np.float64)
+        src = np.asarray(wind_params, dtype=np.float64)
+        wp[:min(steps, len(src)), :3] = src[:steps, :3]
     m = _Model(h, w, vw.ctypes.data, wd.ctypes.data, sl.ctypes.data, ca.ctypes.data,
                de.ctypes.data, float(params.c1), float(params.c2), float(params.a),
                float(params.p_h), float(params.p_continue), float(norm_c),
-               int(factor_site == "source"), int(slope_units == "radians"))
+               int(factor_site == "source"), int(slope_units == "radians"),
+               int(origin[0]), int(origin[1]), None if wp is None else wp.ctypes.data)
     burning = np.empty((h, w), np.uint8)
     burned = np.empty((h, w), np.uint8)
     acc = np.empty((h, w), np.float64)
     t_ign = np.empty((h, w), np.int32)
     jac = np.empty((h, w, 4), np.float64) if want_jac else None
+    jac_abs = np.empty((h, w, 4), np.float64) if (want_jac and want_jac_abs) else None
+    jac_floor = np.empty((h, w, 4), np.float64) if (want_jac and want_jac_abs) else None
+    jac_cond = np.empty((h, w, 4), np.float64) if (want_jac and want_jac_abs) else None
     series = np.zeros((max(steps, 0), 2), np.int64)
     n_ent = C.c_int64(0)
     rc = lib().orc_run(C.byref(m), _ptr(init_u8), int(steps), int(seed) & (2**64 - 1), n_wind,
                        _ptr(wind_at), _ptr(wv), _ptr(wdd), _ptr(attach), int(threads),
                        _ptr(burning), _ptr(burned), _ptr(acc), _ptr(t_ign), _ptr(jac),
-                       _ptr(series), C.byref(n_ent))
+                       _ptr(jac_abs), _ptr(jac_floor), _ptr(jac_cond), _ptr(series),
+                       C.byref(n_ent))
     if rc != 0:
         raise ValueError(f"oracle run failed ({rc})")
     return OracleResult(burning.astype(bool), burned.astype(bool), acc, t_ign, jac, series,
-                        int(n_ent.value))
+                        int(n_ent.value), jac_abs, jac_floor, jac_cond)
 
 
 # ----------------------------------------------------------- tape/loss ---

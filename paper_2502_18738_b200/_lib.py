@@ -53,7 +53,7 @@ class FcLandscape(C.Structure):
 
 class FcShard(C.Structure):
     _fields_ = [("row0", C.c_int32), ("ghost_top", C.c_int32), ("ghost_bottom", C.c_int32),
-                ("pad_", C.c_int32)]
+                ("member0", C.c_int32)]
 
 
 class FcState(C.Structure):

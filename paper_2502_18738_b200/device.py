@@ -224,10 +224,15 @@ class FireBatch:
     steps, per-cell Jacobians, activity flags and per-step counters."""
 
     def __init__(self, shape, members: int = 1, *, max_steps: int = 1024,
-                 with_jacobian: bool = False, device=None):
+                 with_jacobian: bool = False, member0: int = 0, device=None):
+        """member0: global index of local member 0 when an ensemble is
+        sharded over ranks (the member word of the Philox counter)."""
         L.require_cuda()
         dev = _dev(device)
         self.device = dev
+        if member0 < 0:
+            raise ValueError("member0 must be >= 0")
+        self.member0 = int(member0)
         self.h, self.w = int(shape[0]), int(shape[1])
         if self.h < 1 or self.w < 1:
             raise ValueError(f"grid must be at least 1x1, got {shape}")
@@ -375,6 +380,10 @@ class FireBatch:
                 raise ValueError("wind_schedule must be fp64 of shape (max_steps, 4)")
             wind_schedule = wind_schedule.to(self.device).contiguous()
         lst, st = land.struct(), self.struct()
+        if shard is None and self.member0:
+            shard = L.FcShard(0, 0, 0, self.member0)
+        elif shard is not None:
+            shard.member0 = self.member0
         phase = C.c_int32(self.q)
         L.check(L.lib().fc_run(C.byref(self.grid), C.byref(lst), C.byref(st), L.ptr(self.params),
                                L.ptr(self.seeds), mode, L.ptr(draws), self.t, int(nsteps), att,

@@ -49,7 +49,8 @@ class _Slot:
     def __init__(self, runner: "EnsembleRunner", device):
         from . import _lib as L
         r = runner
-        self.batch = FireBatch((r.h, r.w), r.m, max_steps=max(r.steps, 1), device=device)
+        self.batch = FireBatch((r.h, r.w), r.m, max_steps=max(r.steps, 1), member0=r.member0,
+                               device=device)
         dev = self.batch.device
         g = self.batch.grid
         self.env_dev = torch.empty((5, r.h, r.w), dtype=torch.float32, device=dev)
@@ -133,8 +134,11 @@ class EnsembleTicket:
 
 class EnsembleRunner:
     def __init__(self, shape, members: int, steps: int, *, cell_side: float = 30.0,
-                 rng: str = "splitmix", depth: int = 2, device=None):
+                 rng: str = "splitmix", depth: int = 2, member0: int = 0, device=None):
+        """member0: global index of this runner's first member when an
+        ensemble is sharded over ranks (keys the Philox draws)."""
         self.h, self.w = shape
+        self.member0 = int(member0)
         self.m, self.steps, self.rng = int(members), int(steps), rng
         self.cell_side = cell_side
         if depth < 1:
@@ -259,8 +263,11 @@ class EnsembleCalibrator:
         self.land, self.lr, self.wd, self.window = land, lr, weight_decay, window
         self.steps = int(steps if steps is not None else max(obs_steps))
         self.obs = [int(s) for s in obs_steps]
+        members = list(members)
+        if members != list(range(members[0], members[0] + len(members))):
+            raise ValueError("members must be a contiguous block (parallel.shard_members)")
         self.batch = FireBatch(land.shape, len(members), max_steps=self.steps,
-                               with_jacobian=True, device=device)
+                               with_jacobian=True, member0=members[0], device=device)
         dev = self.batch.device
         self.init = init if torch.is_tensor(init) else torch.as_tensor(
             np.asarray(init, dtype=bool).astype(np.uint8), device=dev)

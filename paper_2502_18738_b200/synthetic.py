@@ -113,13 +113,18 @@ def center_ignition(h: int, w: Optional[int] = None, block: int = 3) -> np.ndarr
     return init
 
 
-def random_blocks(h: int, w: int, n: int = 8, block: int = 5, seed: int = 3) -> np.ndarray:
-    """n randomly placed block x block ignitions (config 3)."""
+def random_block_origins(h: int, w: int, n: int = 8, block: int = 5, seed: int = 3):
+    """Top-left cells of random_blocks' ignitions."""
     rng = np.random.default_rng([seed, 0xB10C])
-    init = np.zeros((h, w), dtype=bool)
     rows = rng.integers(block, h - 2 * block, n)
     cols = rng.integers(block, w - 2 * block, n)
-    for r, c in zip(rows, cols):
+    return [(int(r), int(c)) for r, c in zip(rows, cols)]
+
+
+def random_blocks(h: int, w: int, n: int = 8, block: int = 5, seed: int = 3) -> np.ndarray:
+    """n randomly placed block x block ignitions (config 3)."""
+    init = np.zeros((h, w), dtype=bool)
+    for r, c in random_block_origins(h, w, n, block, seed):
         init[r:r + block, c:c + block] = True
     return init
 

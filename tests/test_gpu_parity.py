@@ -164,7 +164,7 @@ def test_calibrate_trajectory_matches_reference():
     np.testing.assert_allclose(rec[:, 2:5], d["records"][:, 2:5], rtol=1e-5)
     traj = np.array([[e, i, p.c1, p.c2, p.a, p.p_h, p.p_continue]
                      for e, i, p in res.manifest.trajectory])
-    np.testing.assert_allclose(traj, d["trajectory"], rtol=1e-4, atol=1e-6)
+    np.testing.assert_allclose(traj, d["trajectory"], rtol=RTOL_GRAD, atol=1e-9)
 
 
 def _oracle_vs_device(size_h, size_w, steps, seed, attach, members=1, env_seed=9, skip=True,
@@ -188,7 +188,7 @@ def test_ragged_grid_members_and_partition_invariance():
     bu, bd = (x.bool().cpu().numpy() for x in b.unpack())
     for m in range(3):
         res = O.run(**arr, params=p, init=init, steps=steps, seed=40 + m,
-                    attach_steps=range(1, steps + 1), threads=4)
+                    attach_steps=range(1, steps + 1), threads=4, want_jac_abs=True)
         assert np.array_equal(bu[m], res.burning) and np.array_equal(bd[m], res.burned)
         np.testing.assert_allclose(b.acc[m].double().cpu().numpy(), res.acc, rtol=RTOL_ACC)
         assert np.array_equal(b.series()[m], res.series)
@@ -197,7 +197,10 @@ def test_ragged_grid_members_and_partition_invariance():
         got = b.contract(torch.as_tensor(np.stack([g * (k == m) for k in range(3)])))[m]
         want = O.contract(res.jac, g)
         np.testing.assert_allclose(got.cpu().numpy(), want, rtol=RTOL_GRAD)
-        np.testing.assert_allclose(jac, res.jac, rtol=2e-4, atol=1e-6)
+        # per-cell J: 1e-5 of its slot terms' scale + the reference's
+        # rounding floor + the fp32 conditioning (tests/test_gpu_envelope.py)
+        tol = RTOL_GRAD * res.jac_abs + res.jac_floor + res.jac_cond
+        assert np.all(np.abs(jac - res.jac) <= tol)
     # dense sweep (no activity skipping) must give identical bytes
     _, _, _, _, b2 = _oracle_vs_device(h, w, steps, 40, True, members=3, skip=False)
     assert torch.equal(b.planes, b2.planes)

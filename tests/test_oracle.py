@@ -200,3 +200,60 @@ def test_calibrate_trajectory_matches_reference():
     np.testing.assert_allclose(traj, d["trajectory"], rtol=1e-9, atol=1e-12)
     np.testing.assert_allclose(best, d["best"], rtol=1e-9)
     assert math.isclose(best_loss, float(d["best_loss"]), rel_tol=1e-9)
+
+
+def _small_env(h, w, seed):
+    from paper_2502_18738_b200 import synthetic as S
+    env = S.make_environment(h, w, seed=seed)
+    return S.reference_landscape_arrays(env, O.slope_from_altitude)
+
+
+def test_oracle_parametric_wind_equals_per_step_updates():
+    # wind_params row t == a WindUpdate (kernel.py:422-428) before 1-based
+    # step t+1 with fields alpha*V + beta, theta + gamma of the base fields
+    arr = _small_env(40, 48, 3)
+    steps = 25
+    rows = np.stack([1.0 + 0.02 * np.arange(steps), 0.1 * np.arange(steps),
+                     3.6 * np.arange(steps)], axis=1)
+    init = np.zeros((40, 48), bool)
+    init[19:22, 23:26] = True
+    p = P([0.045, 0.131, 0.078, 0.58, 0.3])
+    a = O.run(**arr, params=p, init=init, steps=steps, seed=4, wind_params=rows,
+              attach_steps=range(1, steps + 1))
+    upd = [(t + 1, rows[t, 0] * arr["wind_speed"] + rows[t, 1], arr["wind_direction"] + rows[t, 2])
+           for t in range(steps)]
+    b = O.run(**arr, params=p, init=init, steps=steps, seed=4, wind_schedule=upd,
+              attach_steps=range(1, steps + 1))
+    assert np.array_equal(a.burning, b.burning) and np.array_equal(a.burned, b.burned)
+    assert np.array_equal(a.acc, b.acc) and np.array_equal(a.jac, b.jac)
+
+
+def test_oracle_origin_crop_equals_full_domain():
+    # a crop whose border the fire never reaches, run with its absolute
+    # origin, reproduces the full-domain run (draws keyed by absolute cell)
+    arr = _small_env(96, 112, 5)
+    init = np.zeros((96, 112), bool)
+    init[60:63, 70:73] = True
+    p = P([0.045, 0.131, 0.078, 0.58, 0.3])
+    full = O.run(**arr, params=p, init=init, steps=15, seed=9, attach_steps=range(1, 16))
+    r0, r1, c0, c1 = 30, 96, 41, 100
+    aff = full.affected()
+    assert not aff[r0:r0 + 2].any() and not aff[:, c0:c0 + 2].any()
+    crop = {k: (v[r0:r1, c0:c1] if v.ndim == 2 else v[r0:r1, c0:c1]) for k, v in arr.items()}
+    part = O.run(**crop, params=p, init=init[r0:r1, c0:c1], steps=15, seed=9,
+                 attach_steps=range(1, 16), origin=(r0, c0))
+    assert np.array_equal(part.burning, full.burning[r0:r1, c0:c1])
+    assert np.array_equal(part.acc, full.acc[r0:r1, c0:c1])
+    assert np.array_equal(part.jac, full.jac[r0:r1, c0:c1])
+    shifted = O.run(**crop, params=p, init=init[r0:r1, c0:c1], steps=15, seed=9)
+    assert not np.array_equal(shifted.burning, part.burning)
+
+
+def test_oracle_jac_abs_bounds_jac():
+    arr = _small_env(32, 32, 7)
+    init = np.zeros((32, 32), bool)
+    init[15:18, 15:18] = True
+    res = O.run(**arr, params=P([0.045, 0.131, 0.078, 0.58, 0.3]), init=init, steps=10, seed=1,
+                attach_steps=range(1, 11), want_jac_abs=True)
+    assert np.all(res.jac_abs >= np.abs(res.jac) * (1 - 1e-12))
+    assert (res.jac_abs > 0).any()

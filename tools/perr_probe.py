@@ -20,7 +20,7 @@ def f32(bits):
 
 
 def probe(name, dl, shape, members, steps, params, wind=None, attach=False):
-    buf = torch.zeros(8, dtype=torch.int64, device="cuda")
+    buf = torch.zeros(32, dtype=torch.int64, device="cuda")
     b = F.FireBatch(shape, members, max_steps=steps, with_jacobian=attach)
     b.set_params(np.array([F.pack_params(*p) for p in params]))
     b.set_seeds(list(range(members)))
@@ -30,7 +30,10 @@ def probe(name, dl, shape, members, steps, params, wind=None, attach=False):
     torch.cuda.synchronize()
     L.lib().fc_debug_set_trace(None)
     v = buf.cpu().numpy()
-    print(f"{name:40s} decisions {v[1]:>11d}  max |p32-p64| {f32(v[0]):.3e}  max rel {f32(v[2]):.3e}")
+    print(f"{name:40s} decisions {v[1]:>11d}  max |p32-p64| {f32(v[0]):.3e}  max rel {f32(v[2]):.3e}"
+          f"  wide recomputes {v[3]}")
+    # max relative error (p >= FC_GUARD) per slot-magnitude octave eb in [2^(b-3), 2^(b-2))
+    print("    " + "  ".join(f"E<{2.0 ** (b - 2):g}:{f32(v[8 + b]):.1e}" for b in range(24) if v[8 + b]))
 
 
 def main():
@@ -56,6 +59,11 @@ def main():
     probe("rough terrain, 0-30 m/s wind", dl2, (n, n), 4, 200,
           [(0.045, 0.131, 0.078, 0.58, 0.3), (0.2, 0.3, 0.3, 0.9, 0.3),
            (0.0, 0.0, 0.0, 0.3, 0.3), (1.0, 1.0, 1.0, 1.0, 0.3)])
+    probe("rough terrain, attached", dl2, (n, n), 4, 200,
+          [(0.045, 0.131, 0.078, 0.58, 0.3), (0.2, 0.3, 0.3, 0.9, 0.3),
+           (0.0, 0.0, 0.0, 0.3, 0.3), (1.0, 1.0, 1.0, 1.0, 0.3)], attach=True)
+    for c in (0.05, 0.1, 0.2, 0.5):
+        probe(f"rough terrain, a=c1=c2={c}", dl2, (n, n), 4, 200, [(c, c, c, 0.6, 0.4)] * 4)
 
 
 if __name__ == "__main__":
