@@ -216,6 +216,25 @@ int fc_run(const fc_grid* g, const fc_landscape* land, const fc_state* s,
            int32_t skip_inactive, int32_t window, const double* wind_schedule,
            const fc_shard* shard, int32_t* host_phase, fc_stream_t stream);
 
+/* One launch of fc_run on a row shard, split so that the halo exchange of
+ * the previous launch overlaps compute (activity-list sweep, keyed draws;
+ * nsteps <= window steps from pre-step index t0 at launch *host_phase):
+ *   pass 1: the listed tiles outside the boundary tile rows (the first and
+ *           last owned tile rows, next to ghost rows) -- they read no ghost
+ *           rows, so they may run while the ghost rows are being refreshed;
+ *           *host_phase is unchanged;
+ *   pass 2: every tile of the boundary tile rows (a dense sweep of at most
+ *           two tile rows: fire arriving through a ghost row needs no
+ *           activity marks), after the ghost rows hold the neighbours'
+ *           state of this launch's input; advances *host_phase.
+ * Pass 1 then pass 2 of every launch gives the same bytes as fc_run
+ * (kernel.py:307-309 partition invariance; draws keyed by global cells). */
+int fc_run_pass(const fc_grid* g, const fc_landscape* land, const fc_state* s,
+                const double* params, const uint64_t* seeds, int32_t rng_mode, int32_t t0,
+                int32_t nsteps, const uint8_t* host_attach, int32_t window,
+                const double* wind_schedule, const fc_shard* shard, int32_t pass,
+                int32_t* host_phase, fc_stream_t stream);
+
 /* Dense-sweep activity scan for launch `phase` (the first half of every
  * skip_inactive = 0 launch, exposed for measurement): streams the burning
  * plane, lists every tile with fire in its 3x3 tile neighbourhood and writes

@@ -31,7 +31,7 @@ NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", 
 # Every symbol include/firecell.h declares (checked by the CPU test suite).
 EXPORTS = ("fc_grid_make", "fc_plane_words", "fc_loss_workspace_bytes", "fc_state_init",
            "fc_state_reset",
-           "fc_state_unpack", "fc_state_export", "fc_host_device_pointer", "fc_inject", "fc_run", "fc_mark_ghosts", "fc_activity_scan",
+           "fc_state_unpack", "fc_state_export", "fc_host_device_pointer", "fc_inject", "fc_run", "fc_run_pass", "fc_mark_ghosts", "fc_activity_scan",
            "fc_contract", "fc_loss_grad",
            "fc_loss_dense", "fc_adamw", "fc_uniform_grid", "fc_epoch_seed", "fc_build_fields",
            "fc_landscape_build", "fc_landscape_build_ctas",
@@ -109,6 +109,8 @@ def lib():
             "fc_inject": (C.c_int, [G, ST, vp, i32, i32, i32, vp]),
             "fc_run": (C.c_int, [G, LS, ST, vp, vp, i32, vp, i32, i32, vp, i32, i32, vp, SH,
                                  C.POINTER(i32), vp]),
+            "fc_run_pass": (C.c_int, [G, LS, ST, vp, vp, i32, i32, i32, vp, i32, vp, SH, i32,
+                                      C.POINTER(i32), vp]),
             "fc_mark_ghosts": (C.c_int, [G, ST, SH, i32, vp]),
             "fc_activity_scan": (C.c_int, [G, ST, i32, vp]),
             "fc_contract": (C.c_int, [G, ST, vp, i32, vp, vp, vp]),

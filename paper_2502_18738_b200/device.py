@@ -394,6 +394,43 @@ class FireBatch:
         self.q = int(phase.value)
         self._keep = (att_np if attach is not None else None, draws)  # lifetime until sync
 
+    def run_pass(self, land: DeviceLandscape, nsteps: int, window: int, which: int, shard,
+                 *, attach: Optional[Sequence[bool]] = None, rng: str = "splitmix",
+                 wind_schedule: Optional[torch.Tensor] = None, stream=None):
+        """One window launch of a row shard in two passes (fc_run_pass):
+        which = 1 advances the listed tiles away from the ghost rows (the
+        step index and launch phase stay), which = 2 the boundary tile rows
+        (then both advance).  Same bytes as run() on the whole launch."""
+        if which not in (1, 2):
+            raise ValueError("which must be 1 (interior) or 2 (boundary rows)")
+        if not 1 <= nsteps <= window or window not in (1, 4, 8, 16):
+            raise ValueError("a pass covers one launch of 1..window steps")
+        if self.t + nsteps > self.max_steps:
+            raise ValueError(f"run past max_steps={self.max_steps}")
+        if self._mode is False:
+            raise ValueError("split launches need activity lists (skip_inactive=True)")
+        self._mode = True
+        att = None
+        if attach is not None:
+            att_np = np.ascontiguousarray(np.asarray(attach, dtype=np.uint8)[:nsteps])
+            if att_np.any() and self.jac is None:
+                raise ValueError("attached steps need a FireBatch built with_jacobian=True")
+            att = att_np.ctypes.data_as(C.c_void_p)
+        if wind_schedule is not None:
+            if tuple(wind_schedule.shape) != (self.max_steps, 4) or wind_schedule.dtype != torch.float64:
+                raise ValueError("wind_schedule must be fp64 of shape (max_steps, 4)")
+        shard.member0 = self.member0
+        lst, st = land.struct(), self.struct()
+        phase = C.c_int32(self.q)
+        L.check(L.lib().fc_run_pass(C.byref(self.grid), C.byref(lst), C.byref(st),
+                                    L.ptr(self.params), L.ptr(self.seeds), L.RNG_MODES[rng],
+                                    self.t, int(nsteps), att, int(window), L.ptr(wind_schedule),
+                                    C.byref(shard), int(which), C.byref(phase),
+                                    L.stream_ptr(stream)), "fc_run_pass")
+        if which == 2:
+            self.t += int(nsteps)
+            self.q = int(phase.value)
+
     def inject(self, cells, member: int = 0, stream=None):
         """inject_ignitions (kernel.py:405-419) before the current step."""
         rows = []

@@ -1,8 +1,10 @@
-"""Row-sharded single domain (config 3 layout) emulated on one GPU: shards
-exchange ghost tile rows by device copies between window launches; the
-result must equal the unsharded run byte for byte (draws are keyed by the
-global cell).  The multi-process NCCL exchange path is covered on CPU by
-tests/test_parallel_gloo.py."""
+"""Row-sharded single domain (config 3 layout) emulated on one GPU: every
+shard runs on its own stream with the overlapped schedule of the NCCL path
+(sharded.run_overlapped: pass 1 of launch q+1 runs while the ghost rows of
+launch q are refreshed on a communication stream, here by device copies;
+pass 2 waits for them); the result must equal the unsharded run byte for
+byte (draws are keyed by the global cell).  The multi-process exchange and
+schedule are covered on CPU by tests/test_parallel_gloo.py."""
 import numpy as np
 import pytest
 import torch
@@ -14,7 +16,8 @@ from paper_2502_18738_b200.sharded import RowPartition, RowShard, run_sharded_lo
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("world,window,attach", [(2, 8, False), (3, 4, True), (4, 16, False)])
+@pytest.mark.parametrize("world,window,attach", [(2, 8, False), (3, 4, True), (4, 16, False),
+                                                 (2, 1, True), (5, 4, False)])
 def test_row_sharded_equals_unsharded(world, window, attach):
     h, w, steps = 300, 140, 70
     env = S.make_environment(h, w, seed=31)

@@ -10,7 +10,8 @@ import torch
 import torch.multiprocessing as mp
 
 from paper_2502_18738_b200.parallel import allreduce_sum_, shard_members
-from paper_2502_18738_b200.sharded import RowPartition, exchange_halo_tensors
+from paper_2502_18738_b200.sharded import (NcclHalo, RowPartition, RowShard,
+                                           exchange_halo_tensors, run_overlapped)
 
 
 def test_shard_members_partition():
@@ -91,3 +92,75 @@ def test_gloo_allreduce_and_halo_exchange(world):
         p.join(timeout=60)
     assert sorted(r[0] for r in res) == list(range(world))
     assert all(r[1] and r[2] for r in res), res
+
+
+class _FakeBatch:
+    """CPU stand-in for a shard's FireBatch: pass 2 of launch q reads the
+    ghost rows of the launch's input buffers and writes the boundary rows of
+    its output buffers with a value naming (rank, launch, plane)."""
+
+    def __init__(self, shard, rank):
+        self.shard, self.rank = shard, rank
+        self.q, self.device, self.seen = 0, torch.device("cpu"), []
+
+    def run_pass(self, land, n, window, which, fc_shard, stream=None, attach=None):
+        sh = self.shard
+        if which == 1:
+            self.seen.append(("interior", self.q))
+            return
+        p = sh.part
+        self.seen.append(("ghosts", self.q,
+                          [t.clone() for t in sh.ghost("top")] if p.ghost_top else [],
+                          [t.clone() for t in sh.ghost("bottom")] if p.ghost_bottom else []))
+        self.q += 1  # boundary()/ghost() now address this launch's output buffers
+        for which_row in ("first", "last"):
+            for plane, t in enumerate(sh.boundary(which_row)):
+                t.fill_(1000 * self.rank + 10 * (self.q - 1) + plane)
+
+
+def _schedule_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.distributed.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        part = RowPartition(32 * 3 * world, world, rank)
+        sh = object.__new__(RowShard)  # host logic only: no device state
+        sh.part, sh.land, sh.shard = part, None, None
+        t0, t1 = part.owned_tiles
+        sh.rows_tiles = (t1 - t0) + part.ghost_top + part.ghost_bottom
+        sh.tiles_x = 2
+        sh.batch = _FakeBatch(sh, rank)
+        sh.batch.planes = torch.zeros((4, sh.rows_tiles * sh.tiles_x * 32), dtype=torch.int32)
+        run_overlapped([sh], 5 * 4, 4, NcclHalo())
+        ok = True
+        launches = [e for e in sh.batch.seen if e[0] == "ghosts"]
+        ok &= len(launches) == 5 and len(sh.batch.seen) == 10
+        for _, lq, top, bot in launches:
+            # launch lq reads the neighbours' boundary rows of launch lq - 1
+            for plane, t in enumerate(top):
+                want = 0 if lq == 0 else 1000 * (rank - 1) + 10 * (lq - 1) + plane
+                ok &= bool(torch.all(t == want))
+            for plane, t in enumerate(bot):
+                want = 0 if lq == 0 else 1000 * (rank + 1) + 10 * (lq - 1) + plane
+                ok &= bool(torch.all(t == want))
+        q.put((rank, bool(ok)))
+    finally:
+        torch.distributed.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_overlapped_halo_schedule(world):
+    """sharded.run_overlapped with the NCCL exchanger over gloo: every
+    launch's boundary pass sees exactly the neighbours' boundary rows of the
+    previous launch in its ghost rows."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_schedule_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    assert sorted(r[0] for r in res) == list(range(world))
+    assert all(r[1] for r in res), res
