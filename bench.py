@@ -401,7 +401,6 @@ def run_ours(args):
         extras["calibration"] = bench_calibration(dev)
         extras["fig6_sweep"] = bench_fig6_sweep(dev)
         extras["dense_probe"] = bench_dense(dev, peak)
-        extras["c3_single_gpu"] = bench_c3_full(dev)
     cpu = None
     if rank == 0 and world == 1:
         cores = os.cpu_count() or 1
@@ -415,7 +414,7 @@ def run_ours(args):
             "metric": METRIC, "value": value, "unit": "cell-updates/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": float(np.mean(ms)),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic", "config": dict(CONFIG, parallelism=f"member-sharded x{world}"),
+            "data": "synthetic", "config": CONFIG, "parallelism": f"member-sharded x{world}",
             "gpu_launches": launches_per_step * args.steps, "clocks": clocks.summary(),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "affected_cells_final": affected_final,
@@ -548,42 +547,95 @@ def bench_ensemble_calibration(dev, rank, world, members_total=256, iters=3):
             "params_after_c1_c2_a_ph": shared[0, :4].cpu().numpy().tolist()}
 
 
-def bench_row_sharded(dev, rank, world, steps=200, window=8):
-    """Config 3 layout across ranks (weak scaling): each rank owns 2048 rows
-    of a (2048*world) x 16384 domain (sigma x32 env generated on the device,
-    2 random 5x5 ignitions per rank band); K-row halos of both bit planes are
-    exchanged over NCCL after every window launch.  Device time, max over
-    ranks; value = global cell-updates/s."""
+def bench_row_sharded(dev, rank, world, steps=1000, windows=(1, 4, 8)):
+    """Config 3 row-sharded across the ranks, both scalings, with k = 1 (a
+    halo exchange every step) and k = 4 fused steps:
+      strong: the 16384^2 domain split into world row bands;
+      weak:   2048*world x 16384, 2048 rows per rank.
+    8 random 5x5 ignitions in the strong domain (2 per 2048-row band in the
+    weak one), sigma x32 environment generated on the device.  Each window
+    launch is split (fc_run_pass) so the NCCL exchange of its boundary rows
+    overlaps the next launch's interior pass (sharded.run_overlapped).
+    Device time (CUDA events, max over ranks) of the whole run; value =
+    global cell-updates/s.  One rank runs the same domain unsharded
+    (fc_run, activity lists)."""
     import torch
 
+    import paper_2502_18738_b200 as F
     from paper_2502_18738_b200 import synthetic as S
     from paper_2502_18738_b200.parallel import allreduce_max, barrier
     from paper_2502_18738_b200.sharded import RowPartition, RowShard, run_sharded
-    import paper_2502_18738_b200 as F
-    H, Wd = 2048 * world, 16384
-    e = S.make_environment_torch(H, Wd, seed=3, sigma_elev=640.0, sigma_wind=960.0, device=dev)
-    init = torch.as_tensor(S.random_blocks(H, Wd, 2 * world, 5, seed=3).astype(np.uint8),
-                           device=dev)
-    part = RowPartition(H, world, rank)
-    sh = RowShard(part, e["elevation"], e["wind_speed"], e["wind_direction"], e["canopy"],
-                  e["density"], init, max_steps=steps, device=dev)
-    del e
-    sh.batch.set_params(F.pack_params(0.045, 0.131, 0.078, 0.58, 0.3))
-    sh.batch.set_seeds([3])
-    run_sharded(sh, 2 * window, window)  # warm-up (NCCL communicators, caches)
-    sh.batch.reset(sh.batch._init_mask)
-    torch.cuda.synchronize()
-    barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    run_sharded(sh, steps, window)
-    e1.record()
-    torch.cuda.synchronize()
-    ms = allreduce_max(e0.elapsed_time(e1), dev)
-    return {"grid": [H, Wd], "rows_per_rank": 2048, "ranks": world, "steps": steps,
-            "steps_per_launch": window, "cell_updates_per_s": H * Wd * steps / (ms / 1e3),
-            "ms": ms, "halo": "2 bit planes x 1 tile row (32 rows) each way per window, NCCL P2P",
-            "scaling": "weak"}
+    out = {"steps": steps, "ranks": world, "scaling": {"strong": "total work fixed",
+                                                         "weak": "work per rank fixed"},
+           "halo": "2 bit planes x 1 tile row (32 rows) each way per launch, NCCL P2P on a "
+                   "communication stream overlapped with the next launch's interior pass"}
+    for kind in ("strong", "weak"):
+        H, Wd = (16384, 16384) if kind == "strong" else (2048 * world, 16384)
+        nfire = 8 if kind == "strong" else 2 * world
+        e = S.make_environment_torch(H, Wd, seed=3, sigma_elev=640.0, sigma_wind=960.0,
+                                     device=dev)
+        init = torch.as_tensor(S.random_blocks(H, Wd, nfire, 5, seed=3).astype(np.uint8),
+                               device=dev)
+        res = {"grid": [H, Wd], "rows_per_rank": H // world, "ignitions": nfire}
+        if world == 1:
+            land = F.DeviceLandscape.from_elevation(e["elevation"], e["wind_speed"],
+                                                    e["wind_direction"], e["canopy"],
+                                                    e["density"], device=dev)
+            b = F.FireBatch((H, Wd), 1, max_steps=steps, device=dev)
+        else:
+            sh = RowShard(RowPartition(H, world, rank), e["elevation"], e["wind_speed"],
+                          e["wind_direction"], e["canopy"], e["density"], init, max_steps=steps,
+                          device=dev)
+            b = sh.batch
+        del e
+        b.set_params(F.pack_params(0.045, 0.131, 0.078, 0.58, 0.3))
+        b.set_seeds([3])
+        init_local = init if world == 1 else sh.batch._init_mask
+        for k in windows:
+            def one():
+                b.reset(init_local)
+                if world == 1:
+                    b.run(land, steps, window=k)
+                else:
+                    run_sharded(sh, steps, k)
+            b.reset(init_local)  # warm-up: communicators, caches
+            if world == 1:
+                b.run(land, 2 * k, window=k)
+            else:
+                run_sharded(sh, 2 * k, k)
+            torch.cuda.synchronize()
+            # the whole run (reset, every split launch, every halo exchange
+            # on the communication stream) as one CUDA graph: the per-launch
+            # host work (~0.1 ms per window in Python) would otherwise bound
+            # the k = 1 schedule
+            mode = "cuda-graph"
+            try:
+                graph = F.CapturedSequence(one)
+                run = graph.replay
+            except Exception as exc:  # fall back to eager launches, say so
+                torch.cuda.synchronize()
+                mode, run = f"eager (capture failed: {type(exc).__name__})", one
+            barrier()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            run()
+            e1.record()
+            torch.cuda.synchronize()
+            ms = allreduce_max(e0.elapsed_time(e1), dev)
+            res[f"k{k}"] = {"ms": ms, "cell_updates_per_s": H * Wd * steps / (ms / 1e3),
+                            "launch": mode}
+            del run
+            if mode == "cuda-graph":
+                del graph
+        out[kind] = res
+        del b, init
+        if world > 1:
+            del sh
+        else:
+            del land
+        torch.cuda.empty_cache()
+    return out
 
 
 def bench_fig6_sweep(dev, sizes=(200, 1000, 2000, 4000, 8000, 14000), steps=300):
@@ -621,42 +673,6 @@ def bench_fig6_sweep(dev, sizes=(200, 1000, 2000, 4000, 8000, 14000), steps=300)
     return {"steps": steps, "rows": rows,
             "paper": "PyTorchFire: <1 s for maps <1200 (RTX 4090), <=1500 (A800); <60 s at 14000 "
                      "on 'a more advanced GPU'; CPU 300 steps at 1000^2 ~30 s (PAPER.md:456-467)"}
-
-
-def bench_c3_full(dev, steps=1000):
-    """Config 3 at its full length on one GPU: 16384^2, 8 random 5x5
-    ignitions, sigma x32 env, 1000 steps, activity-list sweep, with k = 1
-    (one step per launch, no temporal blocking), k = 4 and k = 8 fused
-    steps.  Device time of the whole run (reset included)."""
-    import torch
-
-    import paper_2502_18738_b200 as F
-    from paper_2502_18738_b200 import synthetic as S
-    n = 16384
-    e = S.make_environment_torch(n, n, seed=3, device=dev)
-    dl = F.DeviceLandscape.from_elevation(e["elevation"], e["wind_speed"], e["wind_direction"],
-                                          e["canopy"], e["density"], device=dev)
-    del e
-    init = torch.as_tensor(S.random_blocks(n, n, 8, 5, seed=3).astype(np.uint8), device=dev)
-    b = F.FireBatch((n, n), 1, max_steps=steps, device=dev)
-    b.set_params(F.pack_params(0.045, 0.131, 0.078, 0.58, 0.3))
-    b.set_seeds([3])
-    out = {"grid": [n, n], "steps": steps, "ignitions": "8 random 5x5 blocks (seed 3)"}
-    for k in (1, 4, 8):
-        b.reset(init)
-        b.run(dl, 2 * k, window=k)  # warm-up
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        b.reset(init)
-        b.run(dl, steps, window=k)
-        e1.record()
-        torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1)
-        out[f"k{k}"] = {"ms": ms, "cell_updates_per_s": n * n * steps / (ms / 1e3)}
-    ser = b.series()
-    out["affected_final"] = int(ser[0, -1].sum())
-    return out
 
 
 def bench_dense(dev, peak):
@@ -731,8 +747,24 @@ def bench_dense(dev, peak):
     return out
 
 
+def spawn_ranks(args) -> bool:
+    """--gpus N > 1 outside torchrun: re-launch this command as N ranks (one
+    process per GPU) through torch.distributed.run; rank 0 prints the line."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return False
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    raise SystemExit(subprocess.call(cmd))
+
+
 def main():
     args = parse()
+    spawn_ranks(args)
     if args.impl == "reference":
         run_reference(args)
     else:

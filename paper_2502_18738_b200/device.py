@@ -279,6 +279,9 @@ class FireBatch:
 
     # ------------------------------------------------------------ plumbing
     def struct(self) -> L.FcState:
+        # the state's buffers never move: build the descriptor once
+        if getattr(self, "_struct", None) is not None:
+            return self._struct
         s = L.FcState()
         base, stride = self.planes.data_ptr(), self.planes.stride(0) * 4
         s.burn0, s.burn1 = base, base + stride
@@ -289,6 +292,7 @@ class FireBatch:
         s.tile_fire = L.ptr(self.tile_fire)
         s.tile_first = L.ptr(self.tile_first)
         s.max_steps = self.max_steps
+        self._struct = s
         return s
 
     def set_params(self, params: Sequence, member: Optional[int] = None):
