@@ -120,6 +120,9 @@ typedef struct {
                                if none: no cell of the tile has t_ign < tile_first.  The
                                loss kernels skip tiles with no ignition before an
                                observation step.  May be NULL (no skipping). */
+    uint8_t* live;          /* [M][H][W] bit k = slot k's neighbour burned pre-step, written
+                               at every ignition (the tape mask of kernel.py:380-383); read
+                               only where t_ign marks an ignition.  May be NULL. */
     int32_t max_steps;
     int32_t pad_;
 } fc_state;
@@ -253,6 +256,26 @@ int fc_mark_ghosts(const fc_grid* g, const fc_state* s, const fc_shard* shard, i
  * workspace: fc_loss_workspace_bytes(g, 1) bytes. */
 int fc_contract(const fc_grid* g, const fc_state* s, const void* dl_dacc, int32_t g_is_f32,
                 double* out, void* workspace, fc_stream_t stream);
+
+/* fp64 recomputation of the ignitions recorded at pre-step indices
+ * t_lo <= t_ign < t_hi (those steps ran on this landscape / wind schedule):
+ * p_ignite and J = dp/d(c1, c2, a, p_h) from the live-slot mask of each cell
+ * (fc_state.live, required), in fp64 with the reference's operation order
+ * (kernel.py:172-190, 232-240; tape.py:134-147).  acc64 [M][H][W] and jac64
+ * [M][H][W][4] (may be NULL) are written for those cells only.  This gives
+ * the pyrocell-signature API fp64 accumulators and tape caches. */
+int fc_recompute64(const fc_grid* g, const fc_landscape* land, const fc_state* s,
+                   const double* params, int32_t t_lo, int32_t t_hi,
+                   const double* wind_schedule, double* acc64, double* jac64,
+                   fc_stream_t stream);
+
+/* backward_params (tape.py:118-148) over a subset of the run's tape blocks:
+ * out[m][4] = sum over cells whose ignition step t_ign has step_flags[t_ign]
+ * != 0 (device uint8 [n_flags]) of dl_dacc (fp64) * jac64 (fc_recompute64),
+ * fixed-order fp64 reduction.  workspace: fc_loss_workspace_bytes(g, 1). */
+int fc_contract_steps(const fc_grid* g, const fc_state* s, const double* dl_dacc,
+                      const double* jac64, const uint8_t* step_flags, int32_t n_flags,
+                      double* out, void* workspace, fc_stream_t stream);
 
 /* combined_loss (losses.py:44-86) summed over n_targets observation steps of
  * one run, fused with the gradient contraction.  acc_s = acc where

@@ -32,7 +32,7 @@ NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", 
 EXPORTS = ("fc_grid_make", "fc_plane_words", "fc_loss_workspace_bytes", "fc_state_init",
            "fc_state_reset",
            "fc_state_unpack", "fc_state_export", "fc_host_device_pointer", "fc_inject", "fc_run", "fc_run_pass", "fc_mark_ghosts", "fc_activity_scan",
-           "fc_contract", "fc_loss_grad",
+           "fc_contract", "fc_recompute64", "fc_contract_steps", "fc_loss_grad",
            "fc_loss_dense", "fc_adamw", "fc_uniform_grid", "fc_epoch_seed", "fc_build_fields",
            "fc_landscape_build", "fc_landscape_build_ctas",
            "fc_last_cuda_error", "fc_version", "fc_debug_set_trace")
@@ -62,7 +62,7 @@ class FcState(C.Structure):
                 ("acc", C.c_void_p), ("t_ign", C.c_void_p), ("jac", C.c_void_p),
                 ("flags", C.c_void_p), ("counters", C.c_void_p), ("tile_list", C.c_void_p),
                 ("list_count", C.c_void_p), ("tile_fire", C.c_void_p), ("tile_first", C.c_void_p),
-                ("max_steps", C.c_int32),
+                ("live", C.c_void_p), ("max_steps", C.c_int32),
                 ("pad_", C.c_int32)]
 
 
@@ -114,6 +114,8 @@ def lib():
             "fc_mark_ghosts": (C.c_int, [G, ST, SH, i32, vp]),
             "fc_activity_scan": (C.c_int, [G, ST, i32, vp]),
             "fc_contract": (C.c_int, [G, ST, vp, i32, vp, vp, vp]),
+            "fc_recompute64": (C.c_int, [G, LS, ST, vp, i32, i32, vp, vp, vp, vp]),
+            "fc_contract_steps": (C.c_int, [G, ST, vp, vp, vp, i32, vp, vp, vp]),
             "fc_loss_grad": (C.c_int, [G, ST, vp, i64, vp, i32, vp, vp, vp, vp, vp, vp]),
             "fc_loss_dense": (C.c_int, [i32, i32, vp, vp, vp, vp, vp, vp, vp]),
             "fc_adamw": (C.c_int, [vp, vp, vp, i32, i32, vp, dbl, dbl, dbl, dbl, dbl, i32, vp, vp]),

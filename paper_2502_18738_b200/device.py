@@ -224,9 +224,12 @@ class FireBatch:
     steps, per-cell Jacobians, activity flags and per-step counters."""
 
     def __init__(self, shape, members: int = 1, *, max_steps: int = 1024,
-                 with_jacobian: bool = False, member0: int = 0, device=None):
+                 with_jacobian: bool = False, member0: int = 0, record_live: bool = False,
+                 device=None):
         """member0: global index of local member 0 when an ensemble is
-        sharded over ranks (the member word of the Philox counter)."""
+        sharded over ranks (the member word of the Philox counter).
+        record_live: keep each ignition's live-slot mask (1 B per cell), which
+        recompute64() turns into fp64 accumulators and Jacobians."""
         L.require_cuda()
         dev = _dev(device)
         self.device = dev
@@ -247,6 +250,8 @@ class FireBatch:
         self.t_ign = torch.empty((self.m, self.h, self.w), dtype=torch.int16, device=dev)
         self.jac = (torch.zeros((self.m, self.h, self.w, 4), dtype=torch.float32, device=dev)
                     if with_jacobian else None)
+        self.live = (torch.zeros((self.m, self.h, self.w), dtype=torch.uint8, device=dev)
+                     if record_live else None)
         self.flags = torch.empty((self.m, self.grid.tiles_y, self.grid.tiles_x), dtype=torch.int32,
                                  device=dev)
         self.max_steps = int(max_steps)
@@ -291,6 +296,7 @@ class FireBatch:
         s.tile_list, s.list_count = L.ptr(self.tile_list), L.ptr(self.list_count)
         s.tile_fire = L.ptr(self.tile_fire)
         s.tile_first = L.ptr(self.tile_first)
+        s.live = L.ptr(self.live)
         s.max_steps = self.max_steps
         self._struct = s
         return s
@@ -505,6 +511,43 @@ class FireBatch:
         am = np.asarray(attach_mask, dtype=bool)
         mask[: min(len(am), self.t)] = am[: self.t]
         return int(cnt[:, mask].sum())
+
+    # ------------------------------------------------------- fp64 outputs
+    def recompute64(self, land: DeviceLandscape, t_lo: int, t_hi: int, acc64: torch.Tensor,
+                    jac64: Optional[torch.Tensor] = None, wind_schedule=None, stream=None):
+        """fc_recompute64: p_ignite (and J) in fp64 for the cells that ignited
+        at pre-step indices [t_lo, t_hi) of this run, which ran on `land`;
+        written into acc64 (M, H, W) / jac64 (M, H, W, 4) fp64 device tensors."""
+        if self.live is None:
+            raise ValueError("recompute64 needs a FireBatch built with record_live=True")
+        for t, shp in ((acc64, (self.m, self.h, self.w)), (jac64, (self.m, self.h, self.w, 4))):
+            if t is not None and (t.dtype != torch.float64 or tuple(t.shape) != shp or
+                                  not t.is_contiguous() or not t.is_cuda):
+                raise ValueError(f"expected a contiguous fp64 {shp} CUDA tensor")
+        st = self.struct()
+        L.check(L.lib().fc_recompute64(C.byref(self.grid), C.byref(land.struct()), C.byref(st),
+                                       L.ptr(self.params), int(t_lo), int(t_hi),
+                                       L.ptr(wind_schedule), L.ptr(acc64), L.ptr(jac64),
+                                       L.stream_ptr(stream)), "fc_recompute64")
+
+    def contract_steps(self, dl_dacc: torch.Tensor, jac64: torch.Tensor, steps,
+                       stream=None) -> torch.Tensor:
+        """backward_params over the ignitions of the given pre-step indices
+        (tape blocks): (M, 4) = sum dL/dacc * J64 (fc_contract_steps)."""
+        g = dl_dacc.to(self.device, torch.float64).reshape(self.m, self.h, self.w).contiguous()
+        flags = torch.zeros((max(self.max_steps, 1),), dtype=torch.uint8)
+        for t in steps:
+            if 0 <= int(t) < flags.numel():
+                flags[int(t)] = 1
+        flags = flags.to(self.device)
+        out = torch.empty((self.m, 4), dtype=torch.float64, device=self.device)
+        st = self.struct()
+        L.check(L.lib().fc_contract_steps(C.byref(self.grid), C.byref(st), L.ptr(g), L.ptr(jac64),
+                                          L.ptr(flags), flags.numel(), L.ptr(out),
+                                          L.ptr(self.workspace), L.stream_ptr(stream)),
+                "fc_contract_steps")
+        self._keep_c = (g, flags)
+        return out
 
     # ----------------------------------------------------------- backward
     def contract(self, dl_dacc: torch.Tensor, stream=None) -> torch.Tensor:

@@ -19,7 +19,7 @@ import torch
 from .device import DEFAULT_NORM_C, NEIGHBOR_POSITIONS, DeviceLandscape, FireBatch, \
     build_fields_device, pack_params
 from .model import FireState, Landscape, ModelParams, new_fire_state
-from .tape import Tape
+from .tape import RunBinding, Tape
 
 # kernel.py:38-47
 OFFSET_BEARINGS = {
@@ -158,26 +158,22 @@ def build_fields(land: Landscape, params: ModelParams, wind=None, *, with_gradie
     return f
 
 
-def _pull_state(batch: FireBatch, state: FireState):
+def _pull_planes(batch: FireBatch, state: FireState):
     b, d = batch.unpack()
     state.burning[...] = b[0].bool().cpu().numpy()
     state.burned[...] = d[0].bool().cpu().numpy()
-    state.accumulator[...] = batch.acc[0].double().cpu().numpy()
 
 
-def _push_state(state: FireState, land_shape, max_steps, with_jac) -> FireBatch:
-    batch = FireBatch(land_shape, 1, max_steps=max_steps, with_jacobian=with_jac)
+def _push_state(state: FireState, land_shape, max_steps) -> FireBatch:
+    batch = FireBatch(land_shape, 1, max_steps=max_steps, record_live=True)
     batch.reset(state.burning, t0=state.t)
-    # burned cells and the previous accumulator come from the host state
-    if state.burned.any() or np.any(state.accumulator != np.where(state.burning, 1.0, 0.0)):
-        _load_full_state(batch, state)
+    if state.burned.any():
+        _load_burned(batch, state)
     return batch
 
 
-def _load_full_state(batch: FireBatch, state: FireState):
-    """Upload an arbitrary host FireState (burned cells, accumulator)."""
-    from .device import L as _L  # noqa: F401
-    words = batch.planes.shape[1]
+def _load_burned(batch: FireBatch, state: FireState):
+    """Upload the burned cells of a host FireState into both burned planes."""
     h, w = batch.h, batch.w
     ty, tx = batch.grid.tiles_y, batch.grid.tiles_x
     burned = np.ones((ty * 32, tx * 32), dtype=bool)   # padding counts as burned
@@ -185,17 +181,38 @@ def _load_full_state(batch: FireBatch, state: FireState):
     bits = np.packbits(burned.reshape(ty, 32, tx, 32).transpose(0, 2, 1, 3), axis=-1,
                        bitorder="little").view(np.uint32).reshape(-1)
     batch.planes[2:4].copy_(torch.from_numpy(bits.view(np.int32)).expand(2, -1))
-    acc = torch.from_numpy(np.asarray(state.accumulator, dtype=np.float32))
-    batch.acc[0].copy_(acc)
     batch.mark_cells_dirty()
-    assert batch.planes.shape[1] == words
+
+
+def _check_fields(fields: PropagationFields, dl: DeviceLandscape, params8, factor_site: str):
+    """step_forward(fields=...) (kernel.py:288-293): the device step derives
+    the per-slot fields from the landscape in fp64 (fc_build_fields, the
+    reference's operation order), so caller fields must be those fields --
+    anything else is refused rather than silently replaced."""
+    if fields.site_is_target != (factor_site == "target"):
+        raise ValueError("fields were built for a different factor_site")
+    want = build_fields_device(dl, params8, False).cpu().numpy()
+    got = np.asarray(fields.fp, dtype=np.float64)
+    h, w = dl.shape
+    if got.shape != want.shape:
+        raise ValueError(f"fields shape {got.shape} != {want.shape}")
+    # targets off the grid are never consumed (kernel.py:117-125)
+    inside = np.zeros((8, h, w), dtype=bool)
+    for k, (pr, pc) in enumerate(NEIGHBOR_POSITIONS):
+        inside[k, max(pr, 0):h + min(pr, 0), max(pc, 0):w + min(pc, 0)] = True
+    if not np.allclose(got[inside], want[inside], rtol=1e-12, atol=0.0):
+        raise ValueError("fields differ from build_fields(land, params): the device step "
+                         "derives its per-slot fields from the landscape")
 
 
 def step_forward(state: FireState, land: Landscape, params: ModelParams, seed: int, *,
                  attach: bool = False, tape: Optional[Tape] = None,
                  fields: Optional[PropagationFields] = None, threads: int = 1, executor=None,
                  norm_c: float = DEFAULT_NORM_C, factor_site: str = "target") -> FireState:
-    """kernel.py:263-333: advance the state one step in place."""
+    """kernel.py:263-333: advance the state one step in place.  The step
+    runs on the device; the ignitions' p_ignite (and J when attached) are
+    recomputed in fp64 (fc_recompute64), so the host accumulator stays fp64
+    like the reference's."""
     if state.shape != land.shape:
         raise ValueError(f"state shape {state.shape} != landscape {land.shape}")
     if attach and tape is None:
@@ -203,14 +220,27 @@ def step_forward(state: FireState, land: Landscape, params: ModelParams, seed: i
     if attach and fields is not None and not fields.has_gradients:
         raise ValueError("attached step needs fields built with_gradients=True")
     dl = _device_landscape(land, factor_site, "degrees")
-    batch = _push_state(state, land.shape, state.t + 1, attach)
-    batch.set_params(_params8(params, norm_c))
+    p8 = _params8(params, norm_c)
+    if fields is not None:
+        _check_fields(fields, dl, p8, factor_site)
+    t = state.t
+    batch = _push_state(state, land.shape, t + 1)
+    batch.set_params(p8)
     batch.set_seeds([seed])
-    batch.run(dl, 1, attach=[attach])
-    _pull_state(batch, state)
+    batch.run(dl, 1)
+    acc64 = torch.as_tensor(np.asarray(state.accumulator, dtype=np.float64),
+                            device=batch.device).reshape(1, *land.shape).contiguous()
+    jac64 = (torch.zeros((1, *land.shape, 4), dtype=torch.float64, device=batch.device)
+             if attach else None)
+    batch.recompute64(dl, t, t + 1, acc64, jac64)
+    _pull_planes(batch, state)
+    state.accumulator[...] = acc64[0].cpu().numpy()
     if attach:
-        tape.accumulate(batch.jac[0], state.t + 1, batch.attached_entries([True]), norm_c)
-    state.t += 1
+        n = int(batch.counters[0, t, 0].item())
+        tape.bind(RunBinding(batch, jac64, acc64, [(t, t + 1, dl, p8, land.wind_speed)], [t + 1],
+                             {t + 1: n}, norm_c, land.canopy, land.density,
+                             factor_site == "target"))
+    state.t = t + 1
     return state
 
 
@@ -234,9 +264,12 @@ def run_simulation(land: Landscape, params: ModelParams, init, steps: int, seed:
                    factor_site: str = "target", slope_units: str = "degrees",
                    rng: str = "splitmix", draws=None) -> SimulationResult:
     """kernel.py:453-529 on the device.  threads is accepted for signature
-    compatibility (results are partition-invariant either way).  Extra
-    keywords: rng ("splitmix" = the reference's draws, "philox", "inject")
-    and draws ((steps, 2, H, W) fp64 uniforms for rng="inject")."""
+    compatibility (results are partition-invariant either way).  The
+    accumulator (and the tape's Jacobians) are recomputed in fp64 from the
+    run's live-slot masks (fc_recompute64), so results keep the reference's
+    fp64 precision.  Extra keywords: rng ("splitmix" = the reference's
+    draws, "philox", "inject") and draws ((steps, 2, H, W) fp64 uniforms for
+    rng="inject")."""
     if steps < 0:
         raise ValueError("steps must be >= 0")
     schedule = sorted(wind_schedule or [], key=lambda u: u.apply_at_step)
@@ -250,14 +283,14 @@ def run_simulation(land: Landscape, params: ModelParams, init, steps: int, seed:
         tape = Tape(land.shape)
     state0 = new_fire_state(init, land)
     dl = _device_landscape(land, factor_site, slope_units)
-    batch = FireBatch(land.shape, 1, max_steps=max(steps, 1), with_jacobian=bool(attach_set))
-    batch.set_params(_params8(params, norm_c))
+    p8 = _params8(params, norm_c)
+    batch = FireBatch(land.shape, 1, max_steps=max(steps, 1), record_live=True)
+    batch.set_params(p8)
     batch.set_seeds([seed])
     batch.reset(state0.burning)
     if draws is not None:
         draws = torch.as_tensor(np.asarray(draws, dtype=np.float64)).reshape(steps, 1, 2, *land.shape)
 
-    attach_flags = np.array([(s in attach_set) for s in range(1, steps + 1)], dtype=bool)
     # segment boundaries: wind updates (applied before their 1-based step)
     # and snapshot points
     cuts = {1, steps + 1}
@@ -266,28 +299,48 @@ def run_simulation(land: Landscape, params: ModelParams, init, steps: int, seed:
         cuts |= {s + 1 for s in range(snapshot_every, steps + 1, snapshot_every)}
     cuts = sorted(c for c in cuts if 1 <= c <= steps + 1)
     pending = list(schedule)
-    snapshots: List[Tuple[int, FireState]] = []
+    vw_now = land.wind_speed
+    segments = []      # (t_lo, t_hi, landscape, params8, wind speed) per run segment
+    snap_planes = []
     for a, b in zip(cuts[:-1], cuts[1:]):
         while pending and pending[0].apply_at_step == a:
             upd = pending.pop(0)
             dl = dl.with_wind(upd.wind_speed, upd.wind_direction)
+            vw_now = upd.wind_speed
         seg_draws = None
         if draws is not None:
             seg_draws = draws[a - 1:b - 1]
-        batch.run(dl, b - a, attach=attach_flags[a - 1:b - 1], rng=rng, draws=seg_draws)
+        batch.run(dl, b - a, rng=rng, draws=seg_draws)
+        segments.append((a - 1, b - 1, dl, p8, vw_now))
         if snapshot_every and (b - 1) % snapshot_every == 0 and b - 1 >= 1:
-            st = FireState(np.zeros(land.shape, bool), np.zeros(land.shape, bool),
-                           np.zeros(land.shape), b - 1)
-            _pull_state(batch, st)
-            snapshots.append((b - 1, st))
+            bu, bd = batch.unpack()
+            snap_planes.append((b - 1, bu[0].bool().cpu().numpy(), bd[0].bool().cpu().numpy()))
+    # p_ignite of every ignition (and J of the attached ones) in fp64
+    acc64 = torch.as_tensor(state0.accumulator, device=batch.device).reshape(1, *land.shape)
+    acc64 = acc64.contiguous()
+    jac64 = (torch.zeros((1, *land.shape, 4), dtype=torch.float64, device=batch.device)
+             if attach_set else None)
+    for t_lo, t_hi, dl_seg, _, _ in segments:
+        batch.recompute64(dl_seg, t_lo, t_hi, acc64, jac64)
     final = FireState(np.zeros(land.shape, bool), np.zeros(land.shape, bool), np.zeros(land.shape),
                       steps)
-    _pull_state(batch, final)
+    _pull_planes(batch, final)
+    final.accumulator[...] = acc64[0].cpu().numpy()
+    snapshots: List[Tuple[int, FireState]] = []
+    if snap_planes:
+        t_ign = batch.t_ign[0].cpu().numpy()
+        for s_, bu, bd in snap_planes:
+            acc_s = np.where(t_ign < s_, final.accumulator, 0.0)
+            snapshots.append((s_, FireState(bu, bd, acc_s, s_)))
     ser = batch.series()[0] if steps > 0 else np.zeros((0, 2), np.int64)
     series = [StepStats(t=i + 1, burning=int(ser[i, 0]), burned=int(ser[i, 1]))
               for i in range(steps)]
     if attach_set:
-        tape.bind(batch, sorted(attach_set), batch.attached_entries(attach_flags), norm_c)
+        cnt = batch.counters[0, :max(steps, 1), 0].cpu().numpy()
+        steps_in = sorted(s for s in attach_set if 1 <= s <= steps)
+        tape.bind(RunBinding(batch, jac64, acc64, segments, steps_in,
+                             {s: int(cnt[s - 1]) for s in steps_in}, norm_c, land.canopy,
+                             land.density, factor_site == "target"))
     res = SimulationResult(state=final, series=series, snapshots=snapshots, tape=tape)
-    res.batch = batch  # device state (t_ign, J) for fused device losses
+    res.batch = batch  # device state (t_ign, live masks)
     return res

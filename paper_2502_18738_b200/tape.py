@@ -2,14 +2,18 @@
 
 The reference records, per attached step, (n, 8) caches of every newly
 ignited cell and contracts them in backward_params (tape.py:118-148).  Here
-the forward kernel writes each attached ignition's Jacobian
-J_j = dp_j/d(c1, c2, a, p_h) once (fp32, HBM), and the backward is a single
-contraction sum_j dL/dacc_j * J_j on the device.  Straight-through semantics
-are unchanged: the realised trajectory is constant (tape.py:1-7).
+the step kernel records each ignition's live-slot mask; fc_recompute64
+turns masks into fp64 p_ignite and J_j = dp_j/d(c1, c2, a, p_h) with the
+reference's operation order, and the backward is one contraction
+sum_j dL/dacc_j * J_j on the device (fc_contract_steps).  The reference's
+TapeBlocks are materialised from the same device record when read.
+Straight-through semantics are unchanged: the realised trajectory is
+constant (tape.py:1-7).
 """
 from __future__ import annotations
 
-from typing import Optional, Tuple
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence, Tuple
 
 import numpy as np
 import torch
@@ -38,73 +42,203 @@ def check_if_attach(step: int, total_steps: int, rings: StepRings) -> bool:
     return step in attachment_plan(total_steps, rings)
 
 
+@dataclass
+class TapeBlock:
+    """tape.py:49-87: one attached step's newly ignited cells, (n, 8) caches
+    over the slot order (zero on dead slots), rows in row-major cell order.
+
+    Blocks of a device run are materialised on demand from the run's
+    live-slot masks and the fp64 fields of the step's landscape
+    (fc_build_fields); p_ignite is the fp64 recomputation fc_recompute64
+    stores in the run's accumulator, so recombine() reproduces it bit for
+    bit, as in the reference."""
+
+    t: int
+    rows: np.ndarray
+    cols: np.ndarray
+    p_ignite: np.ndarray
+    mask: np.ndarray
+    fp: np.ndarray
+    raw: np.ndarray
+    rest: np.ndarray
+    vw: np.ndarray
+    cosm1: np.ndarray
+    slope: np.ndarray
+    veg1: np.ndarray
+    den1: np.ndarray
+    _src: Optional["RunBinding"] = field(default=None, repr=False, compare=False)
+
+    def __len__(self) -> int:
+        return int(self.rows.size)
+
+    def recombine(self) -> np.ndarray:
+        """tape.py:77-87: 1 - prod over slots of (1 - fp), frozen slot order."""
+        factors = np.where(self.mask, 1.0 - self.fp, 1.0)
+        prod = np.ones(len(self), dtype=np.float64)
+        for k in range(8):
+            prod *= factors[:, k]
+        return 1.0 - prod
+
+
+class RunBinding:
+    """The device record of one run's attached steps: the batch (t_ign,
+    live-slot masks), the fp64 Jacobians of its ignitions (fc_recompute64)
+    and the landscape of every step segment, from which TapeBlocks are
+    materialised on demand."""
+
+    def __init__(self, batch, jac64: torch.Tensor, acc64: torch.Tensor, segments,
+                 attached_steps, entries_per_step: dict, norm_c: float, canopy, density,
+                 site_is_target: bool):
+        self.batch, self.jac64, self.acc64 = batch, jac64, acc64
+        self.segments = segments          # [(t_lo, t_hi, DeviceLandscape, params8, wind speed)]
+        self.steps = tuple(int(s) for s in attached_steps)  # 1-based, sorted
+        self.entries = dict(entries_per_step)                # 1-based step -> ignitions
+        self.norm_c = float(norm_c)
+        self.canopy, self.density, self.site_is_target = canopy, density, site_is_target
+        self._blocks: Optional[List[TapeBlock]] = None
+
+    @property
+    def num_entries(self) -> int:
+        return int(sum(self.entries.get(s, 0) for s in self.steps))
+
+    def blocks(self) -> List[TapeBlock]:
+        if self._blocks is None:
+            self._blocks = self._materialise()
+        return self._blocks
+
+    def _materialise(self) -> List[TapeBlock]:
+        from .device import NEIGHBOR_POSITIONS, build_fields_device
+        t_ign = self.batch.t_ign[0]
+        live = self.batch.live[0]
+        h, w = t_ign.shape
+        out = []
+        fields_cache = {}
+        for s in self.steps:
+            t = s - 1
+            if not self.entries.get(s, 0):
+                continue
+            seg = next(g for g in self.segments if g[0] <= t < g[1])
+            key = id(seg[2])
+            if key not in fields_cache:
+                fields_cache.clear()
+                fields_cache[key] = build_fields_device(seg[2], seg[3], with_gradients=True)
+            F = fields_cache[key]
+            idx = torch.nonzero(t_ign == t)  # row-major, as np.nonzero (kernel.py:345-347)
+            rows, cols = idx[:, 0], idx[:, 1]
+            n = rows.numel()
+            bits = live[rows, cols].to(torch.int32)
+            cache = {k: torch.zeros((n, 8), dtype=torch.float64, device=F.device)
+                     for k in ("fp", "raw", "rest", "vw", "cosm1", "slope", "veg1", "den1")}
+            mask = torch.zeros((n, 8), dtype=torch.bool, device=F.device)
+            vw = torch.as_tensor(np.asarray(seg[4], dtype=np.float64), device=F.device)
+            can = torch.as_tensor(np.asarray(self.canopy, dtype=np.float64), device=F.device)
+            den = torch.as_tensor(np.asarray(self.density, dtype=np.float64), device=F.device)
+            for k, (pr, pc) in enumerate(NEIGHBOR_POSITIONS):
+                lv = ((bits >> k) & 1).bool()
+                mask[:, k] = lv
+                sr, sc = (rows + pr)[lv], (cols + pc)[lv]
+                for name, plane in (("fp", 0), ("raw", 8), ("rest", 16), ("cosm1", 24),
+                                    ("slope", 32)):
+                    cache[name][lv, k] = F[plane + k][sr, sc]
+                cache["vw"][lv, k] = vw[sr, sc]
+                site_r, site_c = (rows[lv], cols[lv]) if self.site_is_target else (sr, sc)
+                cache["veg1"][lv, k] = 1.0 + can[site_r, site_c]
+                cache["den1"][lv, k] = 1.0 + den[site_r, site_c]
+            host = {k: v.cpu().numpy() for k, v in cache.items()}
+            out.append(TapeBlock(t=t, rows=rows.cpu().numpy(), cols=cols.cpu().numpy(),
+                                 p_ignite=self.acc64[0][rows, cols].cpu().numpy(),
+                                 mask=mask.cpu().numpy(), _src=self, **host))
+        return out
+
+
 class Tape:
-    """Gradient record of one run: a view of the run's device Jacobians.
+    """tape.py:90-103: append-only record of attached steps.  Entries are
+    device runs (RunBinding: fp64 Jacobians of every attached ignition, the
+    blocks materialised when ``blocks`` is read) or explicit TapeBlocks."""
 
-    num_entries counts ignitions on attached steps (one logical tape entry
-    per ignited cell, as in tape.py:49-103)."""
-
-    def __init__(self, shape):
+    def __init__(self, shape, blocks: Optional[Sequence[TapeBlock]] = None):
         self.shape = tuple(int(v) for v in shape)
-        self.num_entries = 0
-        self.jac: Optional[torch.Tensor] = None   # (H, W, 4) fp32 device
+        self._entries: list = list(blocks) if blocks is not None else []
         self.norm_c: Optional[float] = None
-        self.attached_steps: Tuple[int, ...] = ()
-        self._batch = None
+
+    def add_block(self, block: TapeBlock) -> None:
+        self._entries.append(block)
+
+    def bind(self, binding: RunBinding) -> None:
+        self._entries.append(binding)
+        self.norm_c = binding.norm_c
+
+    @property
+    def blocks(self) -> List[TapeBlock]:
+        out: List[TapeBlock] = []
+        for e in self._entries:
+            out.extend(e.blocks() if isinstance(e, RunBinding) else [e])
+        return out
+
+    @property
+    def num_entries(self) -> int:
+        return int(sum(e.num_entries if isinstance(e, RunBinding) else len(e)
+                       for e in self._entries))
 
     def __len__(self) -> int:
         return self.num_entries
 
-    def bind(self, batch, attached_steps, entries: int, norm_c: float):
-        self._batch = batch
-        self.jac = batch.jac[0]
-        self.attached_steps = tuple(attached_steps)
-        self.num_entries += int(entries)
-        self.norm_c = float(norm_c)
-
-    def accumulate(self, jac: torch.Tensor, step: int, entries: int, norm_c: float):
-        """Add one step's Jacobians (step_forward with attach=True)."""
-        if self.jac is None:
-            self.jac = torch.zeros_like(jac)
-        self.jac += jac
-        self.attached_steps = self.attached_steps + (int(step),)
-        self.num_entries += int(entries)
-        self.norm_c = float(norm_c)
-
 
 def backward_params(tape: Tape, dl_dacc, norm_c: float) -> np.ndarray:
-    """tape.py:118-148 -> (dc1, dc2, da, dp_h)."""
+    """tape.py:118-148 -> (dc1, dc2, da, dp_h), in fp64 on the device: a
+    run's attached steps contract dL/dacc with its fp64 Jacobians
+    (fc_contract_steps, J from fc_recompute64); blocks taken from a run
+    contract the same way over their steps; hand-made blocks use their own
+    caches (the reference's leave-one-out chain)."""
     g = np.asarray(dl_dacc) if not torch.is_tensor(dl_dacc) else dl_dacc
     if tuple(g.shape) != tape.shape:
         raise ValueError(f"loss grid {tuple(g.shape)} != tape grid {tape.shape}")
-    if tape.jac is None or tape.num_entries == 0:
-        return np.zeros(4, dtype=np.float64)
-    from .device import FireBatch  # noqa: F401  (lib loaded by the batch)
-    gt = torch.as_tensor(g, dtype=torch.float64).to(tape.jac.device) if not torch.is_tensor(g) \
-        else g.to(tape.jac.device)
-    # a bound run's plane is valid where its cells ignited (t_ign gates it)
-    tig = tape._batch.t_ign[0] if tape._batch is not None else None
-    out = _contract(tape.jac, gt, tig)
-    # chain_k carries the explicit factor c (tape.py:134-140): rescale when
-    # the caller's constant differs from the forward's
-    scale = float(norm_c) / tape.norm_c if tape.norm_c else 1.0
-    return out * scale
+    grad = np.zeros(4, dtype=np.float64)
+    by_run: dict = {}
+    loose: List[TapeBlock] = []
+    for e in tape._entries:
+        if isinstance(e, RunBinding):
+            by_run.setdefault(id(e), (e, set()))[1].update(s - 1 for s in e.steps)
+        elif e._src is not None:
+            by_run.setdefault(id(e._src), (e._src, set()))[1].add(int(e.t))
+        else:
+            loose.append(e)
+    for run, steps in by_run.values():
+        if not steps:
+            continue
+        gt = torch.as_tensor(g, dtype=torch.float64).to(run.jac64.device) \
+            if not torch.is_tensor(g) else g.to(run.jac64.device, torch.float64)
+        out = run.batch.contract_steps(gt, run.jac64, sorted(steps))[0].cpu().numpy()
+        # the chain carries the explicit factor c (tape.py:134-140)
+        grad += out * (float(norm_c) / run.norm_c)
+    if loose:
+        grad += _blocks_backward(loose, g, norm_c)
+    return grad
 
 
-def _contract(jac: torch.Tensor, g: torch.Tensor, t_ign: Optional[torch.Tensor] = None) -> np.ndarray:
-    import ctypes as C
+def _blocks_backward(blocks: Sequence[TapeBlock], g, norm_c: float) -> np.ndarray:
+    """The reference chain (tape.py:106-148) over hand-made blocks, fp64 on
+    the device."""
     from . import _lib as L
-    h, w = jac.shape[:2]
-    grid = L.grid(h, w, 1)
-    st = L.FcState()
-    st.jac = L.ptr(jac)
-    st.acc = 0
-    st.t_ign = 0 if t_ign is None else L.ptr(t_ign)
-    gg = g.contiguous()
-    ws = torch.empty((max(L.lib().fc_loss_workspace_bytes(C.byref(grid), 1), 4096),),
-                     dtype=torch.uint8, device=jac.device)
-    out = torch.empty((1, 4), dtype=torch.float64, device=jac.device)
-    L.check(L.lib().fc_contract(C.byref(grid), C.byref(st), L.ptr(gg),
-                                1 if gg.dtype == torch.float32 else 0, L.ptr(out), L.ptr(ws),
-                                L.stream_ptr()), "fc_contract")
-    return out[0].cpu().numpy()
+    L.require_cuda()
+    dev = torch.device("cuda")
+    gt = torch.as_tensor(np.asarray(g, dtype=np.float64) if not torch.is_tensor(g) else g,
+                         dtype=torch.float64, device=dev)
+    grad = torch.zeros(4, dtype=torch.float64, device=dev)
+    for b in blocks:
+        if len(b) == 0:
+            continue
+        T = lambda a: torch.as_tensor(np.asarray(a), device=dev)
+        mask, fp = T(b.mask), T(b.fp).double()
+        fac = torch.where(mask, 1.0 - fp, torch.ones_like(fp))
+        pre = torch.cumprod(torch.cat([torch.ones_like(fac[:, :1]), fac[:, :-1]], 1), 1)
+        suf = torch.flip(torch.cumprod(torch.cat([torch.ones_like(fac[:, :1]),
+                                                  torch.flip(fac, [1])[:, :-1]], 1), 1), [1])
+        gv = gt[T(b.rows).long(), T(b.cols).long()]
+        chain = gv[:, None] * (pre * suf) * (norm_c * (1.0 - fp * fp)) * mask
+        raw, vw = T(b.raw).double(), T(b.vw).double()
+        grad[0] += torch.sum(chain * raw * vw)
+        grad[1] += torch.sum(chain * raw * vw * T(b.cosm1).double())
+        grad[2] += torch.sum(chain * raw * T(b.slope).double())
+        grad[3] += torch.sum(chain * T(b.rest).double())
+    return grad.cpu().numpy()

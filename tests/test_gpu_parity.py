@@ -20,6 +20,9 @@ pytestmark = pytest.mark.gpu
 
 RTOL_ACC = 1e-5    # fp32 accumulator vs fp64 reference (north_star)
 RTOL_GRAD = 1e-5   # parameter gradients (north_star)
+# the pyrocell-signature API recomputes p_ignite and J in fp64 (fc_recompute64)
+RTOL_ACC64 = 1e-10
+RTOL_GRAD64 = 1e-9
 
 GOLDEN_DRAWS = {  # pyrocell tests/test_rng.py:7-14
     (0, 0, 0, 0, 0): 0.23286544795475594,
@@ -63,7 +66,9 @@ def test_run_simulation_matches_reference(name):
                            wind_schedule=sched, **kw)
     assert np.array_equal(sim.state.burning, d["burning"])
     assert np.array_equal(sim.state.burned, d["burned"])
-    np.testing.assert_allclose(sim.state.accumulator, d["acc"], rtol=RTOL_ACC, atol=0)
+    # the reference API's accumulator is recomputed in fp64 (fc_recompute64):
+    # it meets the reference to fp64 rounding, far inside the fp32 bar
+    np.testing.assert_allclose(sim.state.accumulator, d["acc"], rtol=RTOL_ACC64, atol=0)
     assert np.array_equal(np.array([[s.burning, s.burned] for s in sim.series]).reshape(-1, 2),
                           d["series"])
     if "grad" in d:
@@ -76,7 +81,7 @@ def test_run_simulation_matches_reference(name):
             if abs(d["grad"][i]) < 1e-12:
                 assert abs(grad[i]) < 1e-10
             else:
-                assert abs(grad[i] - d["grad"][i]) <= RTOL_GRAD * abs(d["grad"][i]), (i, grad, d["grad"])
+                assert abs(grad[i] - d["grad"][i]) <= RTOL_GRAD64 * abs(d["grad"][i]), (i, grad, d["grad"])
 
 
 def test_structural_zero_gradients():
@@ -941,3 +946,49 @@ def test_no_fire_run_and_export():
         f.run(dl, 20, skip_inactive=skip)
         for x, y in zip(_final(b), _final(f)):
             assert torch.equal(x, y)
+
+
+def test_tape_blocks_api():
+    """The reference's TapeBlock API (tape.py:49-103): blocks per attached
+    step in step order, rows row-major, recombine() == p_ignite == the
+    stored accumulator bit for bit, num_entries == ignitions on attached
+    steps, backward_params linear over blocks and over step subsets
+    (pyrocell tests/test_tape.py:61-88, 191-198, 220-244 semantics)."""
+    d = load("run_rand16")
+    land = land_of(d)
+    pr = params_of(d)
+    init = d["init"]
+    steps, seed = int(d["steps"]), int(d["seed"])
+    tape = F.Tape(land.shape)
+    sim = F.run_simulation(land, pr, init, steps, seed, attach_steps=range(1, steps + 1),
+                           tape=tape)
+    blocks = tape.blocks
+    assert [b.t for b in blocks] == sorted(b.t for b in blocks)
+    assert sum(len(b) for b in blocks) == tape.num_entries == \
+        int(sim.state.affected().sum() - np.asarray(init, bool).sum())
+    for b in blocks:
+        order = b.rows * land.shape[1] + b.cols
+        assert np.all(np.diff(order) > 0)
+        assert np.array_equal(b.recombine(), b.p_ignite)
+        assert np.array_equal(b.p_ignite, sim.state.accumulator[b.rows, b.cols])
+        assert np.all(b.mask.any(1)) and np.all(b.fp[~b.mask] == 0.0)
+    _, g = F.combined_loss(sim.state.accumulator, d["target"])
+    full = F.backward_params(tape, g, F.DEFAULT_NORM_C)
+    total = np.zeros(4)
+    for b in blocks:
+        total += F.backward_params(F.Tape(tape.shape, blocks=[b]), g, F.DEFAULT_NORM_C)
+    np.testing.assert_allclose(total, full, rtol=1e-12, atol=1e-15)
+    # hand-made copies of the blocks (no device record) give the same sums
+    loose = [F.TapeBlock(**{k: getattr(b, k) for k in ("t", "rows", "cols", "p_ignite", "mask",
+                                                           "fp", "raw", "rest", "vw", "cosm1",
+                                                           "slope", "veg1", "den1")})
+             for b in blocks]
+    np.testing.assert_allclose(F.backward_params(F.Tape(tape.shape, blocks=loose), g,
+                                                 F.DEFAULT_NORM_C), full, rtol=1e-10)
+    # a run attaching only steps 2 and 5 equals the sum of those blocks
+    part = F.Tape(land.shape)
+    sim2 = F.run_simulation(land, pr, init, steps, seed, attach_steps=[2, 5], tape=part)
+    assert np.array_equal(sim2.state.accumulator, sim.state.accumulator)
+    want = sum(F.backward_params(F.Tape(tape.shape, blocks=[b]), g, F.DEFAULT_NORM_C)
+               for b in blocks if b.t in (1, 4))
+    np.testing.assert_allclose(F.backward_params(part, g, F.DEFAULT_NORM_C), want, rtol=1e-12)
