@@ -3,6 +3,7 @@ declares; host logic (attachment plans, params, AdamW, metrics, schedules)
 matches the reference goldens; device entry points refuse to run without a
 GPU (no CPU fallback)."""
 import math
+import os
 import re
 
 import numpy as np
@@ -12,6 +13,8 @@ import paper_2502_18738_b200 as F
 from paper_2502_18738_b200 import _lib
 from golden_util import meta
 from oracle import oracle as O
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def test_header_and_library_exports():
@@ -122,3 +125,43 @@ def test_device_paths_refuse_cpu():
         F.FireBatch((8, 8))
     with pytest.raises(RuntimeError):
         F.uniform_grid(0, 0, 0, 0, 0, 2, 2)
+
+
+# pyrocell/__init__.py's __all__ (the reference's public API, 0.1.0)
+PYROCELL_ALL = [
+    "AdamWState", "CalibrationResult", "Channel", "DEFAULT_NORM_C", "FireSpreadEstimator",
+    "FireState", "Landscape", "LossBreakdown", "ModelParams", "NEIGHBOR_POSITIONS",
+    "NormCandidate", "Observation", "ObservationSchedule", "PropagationFields", "RunManifest",
+    "SimulationResult", "StepRings", "Tape", "WindUpdate", "adamw_update", "attachment_plan",
+    "backward_params", "build_fields", "calibrate", "check_if_attach", "clamp_params",
+    "combined_loss", "derive_epoch_seed", "fit_normalization_constant", "ignition_prob",
+    "inject_ignitions", "jaccard_index", "manhattan_distance", "new_fire_state",
+    "normalize_prob", "propagate_prob", "run_simulation", "slope_factor", "step_forward",
+    "uniform_draw", "uniform_grid", "validate_landscape", "validate_params", "wind_factor",
+]
+
+
+def test_pyrocell_alias_exposes_the_reference_api():
+    """tools/pyrocell_alias (the harness that runs the reference's own test
+    suite against this package) resolves every public pyrocell name and
+    submodule to this package."""
+    import importlib
+    import sys
+    alias = os.path.join(REPO, "tools", "pyrocell_alias")
+    sys.path.insert(0, alias)
+    try:
+        for k in [k for k in sys.modules if k == "pyrocell" or k.startswith("pyrocell.")]:
+            del sys.modules[k]
+        pyro = importlib.import_module("pyrocell")
+        assert os.path.dirname(pyro.__file__).startswith(alias)
+        for name in PYROCELL_ALL:
+            assert hasattr(pyro, name), name
+        import paper_2502_18738_b200 as F
+        assert pyro.run_simulation is F.run_simulation and pyro.Tape is F.Tape
+        for sub in ("kernel", "model", "rng", "tape", "calibration", "data_io", "cli"):
+            mod = importlib.import_module(f"pyrocell.{sub}")
+            assert mod is importlib.import_module(f"paper_2502_18738_b200.{sub}"), sub
+    finally:
+        sys.path.remove(alias)
+        for k in [k for k in sys.modules if k == "pyrocell" or k.startswith("pyrocell.")]:
+            del sys.modules[k]

@@ -181,8 +181,10 @@ def test_cli_calibrate_matches_reference(tmp_path):
 
 def test_cli_bench_rows(tmp_path):
     out = tmp_path / "bench.csv"
+    assert cli.main(["bench", "--sizes", "64", "--steps", "20", "--out", str(out)]) == 0
+    assert out.read_text().splitlines()[0] == "size,threads,seconds"  # the reference's format
     assert cli.main(["bench", "--sizes", "64,200", "--steps", "30", "--threads", "1,2",
-                     "--out", str(out)]) == 0
+                     "--out", str(out), "--device-times"]) == 0
     rows = out.read_text().splitlines()
     assert rows[0] == "size,threads,seconds,device_seconds"
     assert [r.split(",")[:2] for r in rows[1:]] == [["64", "1"], ["64", "2"], ["200", "1"],
