@@ -35,35 +35,30 @@ def _dev(device) -> torch.device:
     return d
 
 
-def _fast_env(elev, speed, direction, canopy, density) -> torch.Tensor:
-    """fp32 [H][W][4] fast-path record: wind speed, wind vector (east,
-    north) = speed * (cos, sin)(direction), and vd = (1 + canopy)(1 + density)."""
-    rad = direction * (np.pi / 180.0)
-    vd = (1.0 + canopy) * (1.0 + density)
-    return torch.stack([speed, speed * torch.cos(rad), speed * torch.sin(rad), vd],
-                       dim=-1).to(torch.float32).contiguous()
-
-
-def forward_slopes(elev: torch.Tensor, cell_side: float, sign: int = 1) -> torch.Tensor:
-    """fp32 [H][W][4] slope in degrees from each cell toward its E, SW, S, SE
-    neighbour, computed in fp64 like slope_from_altitude (data_io.py:92-132):
-    degrees(atan((E_i - E_j) / (k l))), k = sqrt(2) on diagonals, 0 where the
-    neighbour is off the grid; the opposite directions are exact negations."""
-    e = elev.to(torch.float64)
-    h, w = e.shape
-    out = torch.zeros((h, w, 4), dtype=torch.float64, device=e.device)
-    for j, (dr, dc) in enumerate(((0, 1), (1, -1), (1, 0), (1, 1))):
-        k = math.sqrt(2.0) if dr and dc else 1.0
-        r0, r1 = 0, h - dr
-        c0, c1 = max(-dc, 0), w - max(dc, 0)
-        if r1 <= r0 or c1 <= c0:
-            continue
-        src = e[r0:r1, c0:c1]
-        dst = e[r0 + dr:r1 + dr, c0 + dc:c1 + dc]
-        out[r0:r1, c0:c1, j] = torch.rad2deg(torch.atan((src - dst) / (k * cell_side)))
-    if sign < 0:
-        out = -out
-    return out.to(torch.float32).contiguous()
+def _build_from_rasters(rasters, cell_side: float, sign: int, dev):
+    """fc_landscape_build: (env, slope4, env64, dir32) from five same-shape
+    rasters (elevation, wind speed, wind direction, canopy, density), fp32 or
+    fp64, in one device pass (fp64 arithmetic, the reference's preparation
+    order, data_io.py:92-132 and model.py:76-105)."""
+    ts = [torch.as_tensor(np.asarray(a) if not torch.is_tensor(a) else a) for a in rasters]
+    shape = tuple(ts[0].shape)
+    if len(shape) != 2 or any(tuple(t.shape) != shape for t in ts):
+        raise ValueError("landscape rasters must be 2-D and of one shape")
+    # fp32 rasters stay fp32 (widened exactly in the kernel); anything else
+    # is taken in fp64
+    dt = torch.float32 if all(t.dtype == torch.float32 for t in ts) else torch.float64
+    ts = [t.to(dev, dt).contiguous() for t in ts]
+    h, w = shape
+    env = torch.empty((h, w, 4), dtype=torch.float32, device=dev)
+    slope4 = torch.empty((h, w, 4), dtype=torch.float32, device=dev)
+    env64 = torch.empty((h, w, 5), dtype=torch.float64, device=dev)
+    dir32 = torch.empty((h, w, 2), dtype=torch.float32, device=dev)
+    with torch.cuda.device(dev):
+        L.check(L.lib().fc_landscape_build(
+            h, w, *[L.ptr(t) for t in ts], 1 if dt == torch.float64 else 0, float(cell_side),
+            -1 if sign < 0 else 1, L.ptr(env), L.ptr(slope4), L.ptr(env64), L.ptr(dir32),
+            L.stream_ptr()), "fc_landscape_build")
+    return env, slope4, env64, dir32
 
 
 class DeviceLandscape:
@@ -82,11 +77,13 @@ class DeviceLandscape:
         if factor_site not in ("target", "source"):
             raise ValueError(f"factor_site must be 'target' or 'source', got {factor_site!r}")
         self.env, self.env64 = env.contiguous(), env64.contiguous()
-        self.slope4 = slope4 if slope4 is not None else forward_slopes(
-            self.env64[..., 0], cell_side, -1 if slope_sign < 0 else 1)
-        if dir32 is None:
-            rad = self.env64[..., 2] * (np.pi / 180.0)
-            dir32 = torch.stack([torch.cos(rad), torch.sin(rad)], dim=-1).to(torch.float32)
+        if slope4 is None or dir32 is None:
+            # derived planes from the fp64 rasters (fc_landscape_build)
+            _, s4, _, d32 = _build_from_rasters([self.env64[..., i] for i in range(5)],
+                                                cell_side, slope_sign, self.env64.device)
+            slope4 = s4 if slope4 is None else slope4
+            dir32 = d32 if dir32 is None else dir32
+        self.slope4 = slope4
         self.dir32 = dir32.contiguous()
         self.slope32 = None if slope32 is None else slope32.contiguous()
         self.slope64 = None if slope64 is None else slope64.contiguous()
@@ -107,26 +104,9 @@ class DeviceLandscape:
             raise ValueError(f"unknown slope_sign {slope_sign!r}")
         if cell_side <= 0:
             raise ValueError("cell_side must be > 0")
-        ts = [torch.as_tensor(np.asarray(a) if not torch.is_tensor(a) else a)
-              for a in (elevation, wind_speed, wind_direction, canopy, density)]
-        shape = tuple(ts[0].shape)
-        if len(shape) != 2 or any(tuple(t.shape) != shape for t in ts):
-            raise ValueError("landscape rasters must be 2-D and of one shape")
-        # fp32 rasters stay fp32 (widened exactly in the kernel); anything
-        # else is taken in fp64
-        dt = torch.float32 if all(t.dtype == torch.float32 for t in ts) else torch.float64
-        ts = [t.to(dev, dt).contiguous() for t in ts]
-        h, w = shape
-        env = torch.empty((h, w, 4), dtype=torch.float32, device=dev)
-        slope4 = torch.empty((h, w, 4), dtype=torch.float32, device=dev)
-        env64 = torch.empty((h, w, 5), dtype=torch.float64, device=dev)
-        dir32 = torch.empty((h, w, 2), dtype=torch.float32, device=dev)
         sign = -1 if slope_sign == "uphill-positive" else 1
-        with torch.cuda.device(dev):
-            L.check(L.lib().fc_landscape_build(
-                h, w, *[L.ptr(t) for t in ts], 1 if dt == torch.float64 else 0, float(cell_side),
-                sign, L.ptr(env), L.ptr(slope4), L.ptr(env64), L.ptr(dir32), L.stream_ptr()),
-                "fc_landscape_build")
+        env, slope4, env64, dir32 = _build_from_rasters(
+            (elevation, wind_speed, wind_direction, canopy, density), cell_side, sign, dev)
         return cls(env, env64, cell_side=cell_side, slope_sign=sign, factor_site=factor_site,
                    slope4=slope4, dir32=dir32)
 
@@ -159,17 +139,15 @@ class DeviceLandscape:
         return base
 
     def with_wind(self, wind_speed, wind_direction) -> "DeviceLandscape":
-        """Same landscape with replaced wind fields (WindUpdate, kernel.py:422-428)."""
-        dev = self.env.device
-        v = torch.as_tensor(np.asarray(wind_speed) if not torch.is_tensor(wind_speed) else wind_speed).to(dev, torch.float64)
-        d = torch.as_tensor(np.asarray(wind_direction) if not torch.is_tensor(wind_direction) else wind_direction).to(dev, torch.float64)
-        env64 = self.env64.clone()
-        env64[..., 1], env64[..., 2] = v, d
-        env = _fast_env(env64[..., 0], v, d, env64[..., 3], env64[..., 4])
-        out = DeviceLandscape(env, env64, cell_side=self.cell_side, slope32=self.slope32,
-                              slope64=self.slope64, slope_sign=self.slope_sign,
-                              factor_site=self.factor_site, slope4=self.slope4)
-        return out
+        """Same landscape with replaced wind fields (WindUpdate, kernel.py:422-428),
+        rebuilt by fc_landscape_build (the elevation-derived slope is kept)."""
+        e64 = self.env64
+        env, _, env64, dir32 = _build_from_rasters(
+            (e64[..., 0], wind_speed, wind_direction, e64[..., 3], e64[..., 4]), self.cell_side,
+            self.slope_sign, self.env.device)
+        return DeviceLandscape(env, env64, cell_side=self.cell_side, slope32=self.slope32,
+                               slope64=self.slope64, slope_sign=self.slope_sign,
+                               factor_site=self.factor_site, slope4=self.slope4, dir32=dir32)
 
     def struct(self) -> L.FcLandscape:
         s = L.FcLandscape()

@@ -3,6 +3,7 @@
     model = FireModel(landscape, init)            # a, c1, c2, p_h, p_continue, c
     model.reset(); seed = model.seed
     for step in ...: model.compute(attach=check_if_attach(step, n, rings))
+    (or model.step(attach=...) per step, or model.run(n, rings=rings) fused)
     loss = criterion(model.accumulator, target); loss.backward()
     optimizer.step(); optimizer.zero_grad()
     with torch.no_grad(): model.a.clamp_(0, 1); ...; model.reset(seed=seed)
@@ -119,6 +120,24 @@ class FireModel(nn.Module):
         self._sync_params()
         att = attach if isinstance(attach, (list, tuple, np.ndarray)) else [attach] * steps
         self._batch.run(self._land, steps, attach=att, rng=self._rng)
+
+    def step(self, attach: bool = False):
+        """One CA step (Algorithm 1's inner loop body)."""
+        self.compute(attach=attach, steps=1)
+
+    def run(self, steps: int, attach=False, rings=None):
+        """Advance `steps` steps in fused launches.  attach: one flag for every
+        step, or a per-step sequence; rings (StepRings): attach the steps of
+        attachment_plan(self.t + steps, rings) -- check_if_attach over the
+        whole re-simulation, as in Algorithm 1."""
+        if steps < 0:
+            raise ValueError("steps must be >= 0")
+        if rings is not None:
+            from .tape import attachment_plan
+            total = self.t + steps
+            plan = set(attachment_plan(total, rings))
+            attach = [s in plan for s in range(self.t + 1, total + 1)]
+        self.compute(attach=attach, steps=steps)
 
     @property
     def t(self) -> int:

@@ -573,7 +573,19 @@ def test_landscape_build_kernel_matches_fp64_preparation(dtype):
     ops in the reference's operation order; slope_from_altitude via the
     oracle for the slope field): env64 exact, fp32 fields equal after one
     rounding, off-grid slopes 0, both slope signs."""
-    from paper_2502_18738_b200.device import forward_slopes
+    def forward_slopes(elev, cell_side, sign=1):
+        # fp64 torch restatement of slope_from_altitude's forward pairs
+        # (data_io.py:92-132): toward E, SW, S, SE, 0 off the grid
+        e = elev.to(torch.float64)
+        h, w = e.shape
+        out = torch.zeros((h, w, 4), dtype=torch.float64, device=e.device)
+        for j, (dr, dc) in enumerate(((0, 1), (1, -1), (1, 0), (1, 1))):
+            k = math.sqrt(2.0) if dr and dc else 1.0
+            r1, c0, c1 = h - dr, max(-dc, 0), w - max(dc, 0)
+            src, dst = e[0:r1, c0:c1], e[dr:r1 + dr, c0 + dc:c1 + dc]
+            out[0:r1, c0:c1, j] = torch.rad2deg(torch.atan((src - dst) / (k * cell_side)))
+        return (-out if sign < 0 else out).to(torch.float32)
+
     rng = np.random.default_rng(5)
     h, w = 37, 53
     el = (rng.random((h, w)) * 1500).astype(dtype)
@@ -992,3 +1004,63 @@ def test_tape_blocks_api():
     want = sum(F.backward_params(F.Tape(tape.shape, blocks=[b]), g, F.DEFAULT_NORM_C)
                for b in blocks if b.t in (1, 4))
     np.testing.assert_allclose(F.backward_params(part, g, F.DEFAULT_NORM_C), want, rtol=1e-12)
+
+
+def test_fire_model_algorithm1_reproduces_reference_calibration():
+    """Algorithm 1 driven through the torch FireModel --
+    model.reset(seed), model.step / model.run with check_if_attach,
+    loss.backward(), torch.optim.Adam, clamp_, reset(seed=epoch_seed) --
+    reproduces the parameter trajectory of the reference's own calibrate()
+    (tests/golden/calibrate_small.npz, written by pyrocell) within 1e-5."""
+    from paper_2502_18738_b200.torch_model import FireModel, combined_loss_torch
+    d = load("calibrate_small")
+    size = int(d["size"])
+    env = S.make_environment(size, seed=5)
+    arr = S.reference_landscape_arrays(env, O.slope_from_altitude)
+    dl = F.DeviceLandscape.from_slope_tensor(arr["wind_speed"], arr["wind_direction"],
+                                             arr["slope"], arr["canopy"], arr["density"])
+    targets = [torch.as_tensor(t) for t in d["targets"]]
+    rings, interval = F.StepRings(1, 2, 3), 6
+    model = FireModel(dl, S.center_ignition(size), c1=0.0, c2=0.0, a=0.0, p_h=0.3,
+                      p_continue=0.5, seed=0)
+    opt = torch.optim.Adam([model.c_1, model.c_2, model.a, model.p_h], lr=0.05)
+    traj = []
+    for epoch in range(1, 4):
+        epoch_seed = F.derive_epoch_seed(5, epoch)
+        model.reset(seed=epoch_seed)
+        for it in range(1, len(targets) + 1):
+            n = it * interval
+            if it % 2:  # per-step calls, as written in Algorithm 1
+                for step in range(1, n + 1):
+                    model.step(attach=F.check_if_attach(step, n, rings))
+            else:       # the fused form
+                model.run(n, rings=rings)
+            loss = combined_loss_torch(model.accumulator, targets[it - 1])
+            loss.backward()
+            opt.step()
+            opt.zero_grad()
+            model.clamp_()
+            traj.append([epoch, it, model.c_1.item(), model.c_2.item(), model.a.item(),
+                         model.p_h.item(), model.p_continue.item()])
+            model.reset(seed=epoch_seed)
+    np.testing.assert_allclose(np.array(traj), d["trajectory"], rtol=RTOL_GRAD, atol=1e-9)
+
+
+def test_wind_swap_rebuilds_with_the_landscape_kernel():
+    """DeviceLandscape.with_wind (WindUpdate, FireModel.wind) goes through
+    fc_landscape_build: the result equals a landscape built from scratch
+    with the new wind, plane for plane; the constructor's derived planes
+    come from the same kernel."""
+    env = S.make_environment(64, 48, seed=8)
+    dl = F.DeviceLandscape.from_environment(env)
+    rng = np.random.default_rng(3)
+    v2 = rng.uniform(0, 12, (64, 48))
+    d2 = rng.uniform(0, 360, (64, 48))
+    swapped = dl.with_wind(v2, d2)
+    fresh = F.DeviceLandscape.from_elevation(env.elevation.astype(np.float64), v2, d2,
+                                             env.canopy.astype(np.float64),
+                                             env.density.astype(np.float64))
+    for name in ("env", "env64", "dir32", "slope4"):
+        assert torch.equal(getattr(swapped, name), getattr(fresh, name)), name
+    bare = F.DeviceLandscape(fresh.env, fresh.env64)
+    assert torch.equal(bare.slope4, fresh.slope4) and torch.equal(bare.dir32, fresh.dir32)
