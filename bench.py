@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-extras", action="store_true", help="skip calibration/dense probes")
     ap.add_argument("--cpu-sample-steps", type=int, default=500)
+    ap.add_argument("--pyrocell-steps", type=int, default=300,
+                    help="steps of the pyrocell (reference itself) CPU sample")
     return ap.parse_args()
 
 
@@ -178,6 +180,54 @@ def cpu_sample(env, members, steps, threads):
         O.run(**arr, params=p, init=init, steps=steps, seed=m, threads=threads, want_jac=False)
     dt = time.perf_counter() - t0
     return len(members) * H * W * steps / dt, dt
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def pyrocell_sample(env, steps, threads_list):
+    """pyrocell 0.1.0 itself (the reference, pure NumPy, installed in
+    baseline/_ref) on member 0 of the c1 workload: its own
+    slope_from_altitude and run_simulation on the same fp32 rasters, bbox
+    windowing on, for each thread count; cell-updates/s (full-grid)."""
+    ref = os.path.join(REPO, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "pyrocell")):
+        return {"unavailable": "baseline/_ref/pyrocell not installed"}
+    sys.path.insert(0, ref)
+    try:
+        import pyrocell as P
+        from pyrocell.data_io import slope_from_altitude
+    finally:
+        sys.path.remove(ref)
+    if not os.path.dirname(P.__file__).startswith(ref):
+        return {"unavailable": f"imported pyrocell from {P.__file__}, not baseline/_ref"}
+    from paper_2502_18738_b200 import synthetic as S
+    f64 = lambda a: np.asarray(a, dtype=np.float64)
+    land = P.Landscape(wind_speed=f64(env.wind_speed), wind_direction=f64(env.wind_direction),
+                       slope=slope_from_altitude(f64(env.elevation), env.cell_side),
+                       canopy=f64(env.canopy), density=f64(env.density), cell_side=env.cell_side)
+    ph = float(S.ensemble_ph(MEMBERS)[0])
+    params = P.ModelParams(c1=0.045, c2=0.131, a=0.078, p_h=ph, p_continue=0.3)
+    init = S.center_ignition(H)
+    out = {"cpu_model": cpu_model(), "numpy": np.__version__,
+           "sample": f"member 0 of c1: 1 x {H}^2 x {steps} steps, pyrocell.run_simulation "
+                     f"(fp64, bbox window, row-band threads)"}
+    for th in threads_list:
+        t0 = time.perf_counter()
+        P.run_simulation(land, params, init, steps, 0, threads=th)
+        dt = time.perf_counter() - t0
+        out[f"threads_{th}"] = {"value": H * W * steps / dt, "unit": "cell-updates/s",
+                                "seconds": dt}
+    return out
 
 
 def run_reference(args):
@@ -407,7 +457,11 @@ def run_ours(args):
         v, dt = cpu_sample(env, [0], args.cpu_sample_steps, cores)
         cpu = {"value": v, "unit": "cell-updates/s", "cores": cores, "kind": "port",
                "sample": f"member 0 of c1: 1 x {H}^2 x {args.cpu_sample_steps} steps, oracle port "
-                         f"(fp64, bbox window, OpenMP), {dt:.1f} s"}
+                         f"(fp64, bbox window, OpenMP), {dt:.1f} s",
+               "cpu_model": cpu_model(),
+               # the reference itself beside the port: pyrocell
+               # with one thread and with every core
+               "reference_pyrocell": pyrocell_sample(env, args.pyrocell_steps, (1, cores))}
 
     if rank == 0:
         line = {

@@ -112,9 +112,17 @@ class EnsembleTicket:
 
     def __init__(self, slot: _Slot, steps: int):
         self.slot, self.steps, self.event = slot, steps, slot.copied
+        self.inputs_consumed = slot.uploaded  # the H2D copies of this call's inputs are done
 
     def done(self) -> bool:
         return self.event.query()
+
+    def wait_inputs(self) -> None:
+        """Block until this call has read the caller's host input buffers
+        (env_host, init_host): only then may the caller refill them.  submit()
+        returns before the asynchronous copies run (that is what lets the
+        upload overlap the previous call's kernels)."""
+        self.inputs_consumed.synchronize()
 
     def result(self) -> EnsembleResult:
         self.event.synchronize()
@@ -185,6 +193,9 @@ class EnsembleRunner:
         """Queue one call.  env_host: (5, H, W) fp32 (elevation, speed,
         direction, canopy, density), ideally pinned; init_host: (H, W)
         uint8/bool; params: per-member (c1, c2, a, p_h, p_continue).
+        The host inputs are read asynchronously: a caller that refills the
+        same buffers for the next call must first wait for
+        ``ticket.wait_inputs()`` (or ``result()``).
 
         Streams: uploads and the landscape build on upload_stream,
         overlapping the previous call's kernels; the device
@@ -215,6 +226,9 @@ class EnsembleRunner:
                 st.wait_stream(caller)
                 slot.graph = CapturedSequence(slot.device_part)
         with torch.cuda.stream(us):
+            # inputs the caller produced on its stream (device-side writes to
+            # pinned buffers, or a preceding call's results) come first
+            us.wait_stream(caller)
             if slot.computed is not None:
                 us.wait_event(slot.computed)   # its previous run has read the inputs
             slot.env_dev.copy_(env_host, non_blocking=True)

@@ -1064,3 +1064,41 @@ def test_wind_swap_rebuilds_with_the_landscape_kernel():
         assert torch.equal(getattr(swapped, name), getattr(fresh, name)), name
     bare = F.DeviceLandscape(fresh.env, fresh.env64)
     assert torch.equal(bare.slope4, fresh.slope4) and torch.equal(bare.dir32, fresh.dir32)
+
+
+def test_ensemble_runner_refilled_pinned_inputs():
+    """The documented pattern of one pinned input buffer refilled between
+    pipelined submits: after ticket.wait_inputs() the buffer may
+    be rewritten, and every call's result is that of its own inputs."""
+    from paper_2502_18738_b200.ensemble import EnsembleRunner
+    n, m, steps = 128, 2, 40
+    envs = [S.make_environment(n, seed=s) for s in (21, 22, 23)]
+    host = lambda e: torch.stack([torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32))
+                                  for a in (e.elevation, e.wind_speed, e.wind_direction,
+                                            e.canopy, e.density)])
+    env_host = torch.empty((5, n, n), dtype=torch.float32).pin_memory()
+    init_host = torch.from_numpy(S.center_ignition(n).astype(np.uint8)).pin_memory()
+    params = [(0.05, 0.12, 0.08, 0.6, 0.4)] * m
+    r = EnsembleRunner((n, n), m, steps, depth=2)
+    tickets = []
+    for e in envs:
+        env_host.copy_(host(e))
+        t = r.submit(env_host, init_host, params, [1, 2])
+        t.wait_inputs()          # the buffer may be refilled from here on
+        tickets.append(t)
+    # results of the first two calls are read before their slots are reused
+    got = []
+    for t in tickets:
+        res = t.result()
+        got.append((res.burning.copy(), res.accumulator.copy()))
+    # the last slot is still valid; earlier ones were overwritten by later
+    # submits, so compare each call with a direct device run
+    for e, (bu_h, acc_h), t in zip(envs[1:], got[1:], tickets[1:]):
+        dl = F.DeviceLandscape.from_environment(e)
+        b = F.FireBatch((n, n), m, max_steps=steps)
+        b.set_params(np.array([F.pack_params(*p) for p in params]))
+        b.set_seeds([1, 2])
+        b.reset(S.center_ignition(n))
+        b.run(dl, steps)
+        np.testing.assert_array_equal(bu_h, b.unpack()[0].cpu().numpy())
+        np.testing.assert_array_equal(acc_h, b.acc.cpu().numpy())
