@@ -375,31 +375,61 @@ def run_ours(args):
     # cell-updates the launches process / their CUDA-event time.  8(d):
     # B(M, k) = (16/M + 2)/k B per cell-update (16 B of fp32 env shared by M
     # members, 1 B state read + 1 B written, once per k fused steps).
+    # the window kernel's time INSIDE the timed timeline: the same graph
+    # replayed (reset + every PDL-chained window launch) minus a graph of the
+    # reset alone, over the window launches -- CUDA events on the launching
+    # stream, L2 flushed as in the timed loop
+    reset_graph = F.CapturedSequence(lambda: batch.reset(init_dev))
+    for _ in range(args.warmup):
+        reset_graph.replay()
+    ms_reset = timed_loop(reset_graph.replay, args.steps, flush)
+    ms_full = timed_loop(graph.replay, args.steps, flush)
+    win_ms = float(np.mean(ms_full) - np.mean(ms_reset))
+    avg_us = 1e3 * win_ms / nwin
     lms, lbytes, cnt = per_launch_profile(batch, dl, STEPS, WINDOW)
     b_cu = (16.0 / MEMBERS + 2.0) / WINDOW
     run_cu = MEMBERS * H * W * STEPS
-    achieved = b_cu * run_cu / (lms.sum() / 1e3) / 1e9
-    kern = float(lbytes.sum() / (lms.sum() / 1e3)) / 1e9
+    alg_per_launch = b_cu * run_cu / nwin
+    achieved = alg_per_launch / (avg_us / 1e6) / 1e9
+    kern = float(lbytes.mean()) / (avg_us / 1e6) / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
-                "kernel": f"window_kernel<SPLITMIX,elev,no-attach,K={WINDOW}>",
-                "avg_launch_us": float(1e3 * lms.mean()), "launches": int(len(lms)),
+                "kernel": f"window_kernel<SPLITMIX,elev,no-attach,K={WINDOW},G=8>",
+                "avg_launch_us": avg_us, "launches": nwin,
+                "avg_launch_timing": "in the timed graph: (reset + all window launches) minus "
+                                     "(reset alone), CUDA events, / launches; the windows' share "
+                                     f"of the step is {win_ms / float(np.mean(ms_full)):.3f}",
+                "avg_launch_us_standalone": float(1e3 * lms.mean()),
                 "algorithmic_bytes_per_cell_update": b_cu,
-                "algorithmic_bytes_per_launch": b_cu * run_cu / len(lms),
+                "algorithmic_bytes_per_launch": alg_per_launch,
+                "meaning": "dense-equivalent: SURVEY 8(d) B(M=16,k=8)=0.375 B per cell-update "
+                           "over every cell of every member, whether or not the kernel visits "
+                           "it (activity skipping visits ~1900 of 65536 tiles per launch)",
                 "kernel_bytes_per_launch": float(lbytes.mean()),
                 "kernel_bytes_GBps": kern, "kernel_bytes_frac": kern / peak,
-                "tiles_visited_per_launch": float(cnt[::WINDOW, 2].mean()),
-                "note": "achieved/frac: SURVEY 8(d) B(M=16,k=8)=0.375 B/cell-update over every "
-                        "cell of every member; the kernel itself touches only tiles near fire "
-                        "(kernel_bytes: 512 B per visited 32x32 tile + 16 B env per work item "
-                        "+ 6 B per ignition), so its own traffic is far below the 8(d) figure "
-                        "and it is latency-bound (DESIGN.md 3)"}
+                "tiles_visited_per_launch": float(cnt[::WINDOW, 2].mean())}
     prof = os.path.join(REPO, "profiles", "ncu_traffic.json")
     if os.path.exists(prof):
         with open(prof) as f:
             tr = json.load(f)
-        roofline["traffic"] = tr.get("c1_step_kernel_dram_bytes_per_launch")
+        dram = tr.get("c1_step_kernel_dram_bytes_per_launch")
+        inst = tr.get("c1_step_kernel_warp_instructions_per_launch")
+        roofline["traffic"] = dram
         roofline["traffic_source"] = tr.get("source")
+        if dram:
+            gbs = dram / (avg_us / 1e6) / 1e9
+            # what the kernel really moves to and from HBM (ncu dram bytes)
+            roofline["hbm_measured"] = {"GBps": gbs, "frac_of_measured_peak": gbs / peak,
+                                        "frac_of_8TBps_spec": gbs / 8000.0}
+        if inst:
+            clk = 1.965e9
+            floor_us = inst / (148 * 4 * clk) * 1e6  # 4 issue slots per SM per clock
+            roofline["issue_roofline"] = {
+                "warp_instructions_per_launch": inst, "issue_floor_us": floor_us,
+                "frac": floor_us / avg_us,
+                "note": "148 SMs x 4 schedulers x 1 warp-instruction/clock at 1965 MHz; the "
+                        "kernel is latency-bound (barrier and memory-latency stalls), "
+                        "profiles/r2_ncu_summary.md"}
     # -------------------------------------------------------------- e2e
     runner = EnsembleRunner((H, W), MEMBERS, STEPS, device=dev)
     env_host = torch.stack([torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)) for a in
@@ -773,22 +803,25 @@ def bench_dense(dev, peak):
             import ctypes as C
             from paper_2502_18738_b200 import _lib as L
             st = b.struct()
-            evs = []
-            for _ in range(20):
-                b.list_count.zero_()
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record()
-                L.check(L.lib().fc_activity_scan(C.byref(b.grid), C.byref(st), b.q, L.stream_ptr()),
-                        "fc_activity_scan")
-                e1.record()
-                evs.append((e0, e1))
+            scan = lambda: L.check(L.lib().fc_activity_scan(C.byref(b.grid), C.byref(st), b.q,
+                                                            L.stream_ptr()), "fc_activity_scan")
+            # 20 back-to-back scans in one CUDA graph (as in the dense sweep,
+            # where each follows a window launch): launch overhead amortised
+            g20 = F.CapturedSequence(lambda: [scan() for _ in range(20)])
+            g20.replay()
             torch.cuda.synchronize()
-            sms = np.array([a.elapsed_time(c) for a, c in evs[2:]])
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(5):
+                g20.replay()
+            e1.record()
+            torch.cuda.synchronize()
+            us = e0.elapsed_time(e1) * 1e3 / 100
             tiles = n * n // 1024
             live = int(b.list_count[b.q].item())
             sbytes = 128.0 * tiles + 128.0 * (tiles - live)  # plane read + quiet tiles' zero writes
-            ach_s = sbytes / (sms.mean() / 1e3) / 1e9
-            out["dense"]["activity_scan"] = {"avg_us": float(1e3 * sms.mean()),
+            ach_s = sbytes / (us / 1e6) / 1e9
+            out["dense"]["activity_scan"] = {"avg_us": us, "timing": "20 scans per CUDA graph",
                                              "bytes": sbytes, "achieved_GBps": ach_s,
                                              "frac_of_peak": ach_s / peak, "live_tiles": live}
         del b
