@@ -22,8 +22,9 @@
  *                 step parity (burn[t & 1] holds pre-step-t state); burned is
  *                 updated in place.  Padding cells outside HxW are "burned".
  *   accumulator   fp32 [M][H][W]; t_ign int16 [M][H][W] (pre-step index of
- *                 the step a cell ignited in; -1 initial/injected; 0x7FFF
- *                 never); jacobian fp32 [M][H][W][4] = dp/d(c1,c2,a,p_h)
+ *                 the step a cell ignited in, minus fc_state.t_base; -1
+ *                 initial/injected or before the base; 0x7FFF never);
+ *                 jacobian fp32 [M][H][W][4] = dp/d(c1,c2,a,p_h)
  *                 captured at ignition on attached steps (0 elsewhere).
  *   landscape     env fp32 [H][W][4] = {wind speed m/s, wind vector east and
  *                 north m/s (speed * cos/sin of the direction, deg East-CCW),
@@ -124,7 +125,9 @@ typedef struct {
                                at every ignition (the tape mask of kernel.py:380-383); read
                                only where t_ign marks an ignition.  May be NULL. */
     int32_t max_steps;
-    int32_t pad_;
+    int32_t t_base;         /* t_ign and tile_first hold (pre-step index - t_base): int16
+                               t_ign spans 32766 steps from the base, and runs longer than
+                               that move the base forward with fc_state_rebase */
 } fc_state;
 
 /* Position of this state in a partitioned job.  Row-sharded single domain
@@ -187,6 +190,13 @@ int fc_state_export(const fc_grid* g, const fc_state* s, int32_t phase, uint8_t*
 
 /* Device address of pinned host memory (cudaHostGetDevicePointer). */
 int fc_host_device_pointer(void* host, void** device_ptr);
+
+/* Long runs (kernel.py:453-468 has no step limit): every recorded ignition
+ * becomes "before the base" (t_ign -1, tile_first -1); the caller then moves
+ * fc_state.t_base to the current pre-step index, after which t_ign counts
+ * steps from there.  Losses, contractions and fp64 recomputation address
+ * ignitions after the last rebase only (recompute64 before rebasing). */
+int fc_state_rebase(const fc_grid* g, const fc_state* s, fc_stream_t stream);
 
 /* inject_ignitions (kernel.py:405-419) before pre-step t (launch phase
  * `phase`): cells is int32 [n][3] = (member, row, col), all in bounds

@@ -31,7 +31,7 @@ NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", 
 # Every symbol include/firecell.h declares (checked by the CPU test suite).
 EXPORTS = ("fc_grid_make", "fc_plane_words", "fc_loss_workspace_bytes", "fc_state_init",
            "fc_state_reset",
-           "fc_state_unpack", "fc_state_export", "fc_host_device_pointer", "fc_inject", "fc_run", "fc_run_pass", "fc_mark_ghosts", "fc_activity_scan",
+           "fc_state_unpack", "fc_state_export", "fc_state_rebase", "fc_host_device_pointer", "fc_inject", "fc_run", "fc_run_pass", "fc_mark_ghosts", "fc_activity_scan",
            "fc_contract", "fc_recompute64", "fc_contract_steps", "fc_loss_grad",
            "fc_loss_dense", "fc_adamw", "fc_uniform_grid", "fc_epoch_seed", "fc_build_fields",
            "fc_landscape_build", "fc_landscape_build_ctas",
@@ -63,7 +63,7 @@ class FcState(C.Structure):
                 ("flags", C.c_void_p), ("counters", C.c_void_p), ("tile_list", C.c_void_p),
                 ("list_count", C.c_void_p), ("tile_fire", C.c_void_p), ("tile_first", C.c_void_p),
                 ("live", C.c_void_p), ("max_steps", C.c_int32),
-                ("pad_", C.c_int32)]
+                ("t_base", C.c_int32)]
 
 
 def build(force: bool = False) -> str:
@@ -107,6 +107,7 @@ def lib():
             "fc_state_export": (C.c_int, [G, ST, i32, vp, vp, vp, vp, vp]),
             "fc_host_device_pointer": (C.c_int, [vp, C.POINTER(vp)]),
             "fc_inject": (C.c_int, [G, ST, vp, i32, i32, i32, vp]),
+            "fc_state_rebase": (C.c_int, [G, ST, vp]),
             "fc_run": (C.c_int, [G, LS, ST, vp, vp, i32, vp, i32, i32, vp, i32, i32, vp, SH,
                                  C.POINTER(i32), vp]),
             "fc_run_pass": (C.c_int, [G, LS, ST, vp, vp, i32, i32, i32, vp, i32, vp, SH, i32,

@@ -217,8 +217,6 @@ class FireBatch:
         self.h, self.w = int(shape[0]), int(shape[1])
         if self.h < 1 or self.w < 1:
             raise ValueError(f"grid must be at least 1x1, got {shape}")
-        if max_steps >= L.T_NEVER - 1:
-            raise ValueError(f"max_steps must be < {L.T_NEVER}")
         self.m = int(members)
         self.grid = L.grid(self.h, self.w, self.m)
         words = L.lib().fc_plane_words(C.byref(self.grid))
@@ -251,6 +249,7 @@ class FireBatch:
         ws = max(L.lib().fc_loss_workspace_bytes(C.byref(self.grid), 8), 1 << 12)
         self.workspace = torch.empty((ws,), dtype=torch.uint8, device=dev)
         self.t = 0
+        self.t_base = 0  # t_ign / tile_first count steps from here (fc_state.t_base)
         self.q = 0  # launches since reset (burning-buffer parity, activity lists)
         self._init_burning_dev = torch.zeros((self.m,), dtype=torch.int64, device=dev)
         self._hw = hw
@@ -276,6 +275,7 @@ class FireBatch:
         s.tile_first = L.ptr(self.tile_first)
         s.live = L.ptr(self.live)
         s.max_steps = self.max_steps
+        s.t_base = self.t_base
         self._struct = s
         return s
 
@@ -323,8 +323,28 @@ class FireBatch:
                    L.stream_ptr(stream)), "fc_state_init")
         self._cells_clean = True
         self.t = int(t0)
+        self._set_base(int(t0))
         self.q = 0
         self._mode = None
+
+    # --------------------------------------------------------- long runs
+    REBASE_SPAN = 30000  # steps between bases (int16 t_ign spans 32766)
+
+    def _set_base(self, t_base: int):
+        self.t_base = int(t_base)
+        if getattr(self, "_struct", None) is not None:
+            self._struct.t_base = self.t_base
+
+    def rebase(self, stream=None):
+        """fc_state_rebase: ignitions recorded so far count as "before the
+        base" (t_ign -1) and the base moves to the current step, so runs may
+        exceed the int16 ignition-step range (kernel.py:453-468 has no step
+        limit).  Losses, tape steps and recompute64 then address ignitions
+        after this point only."""
+        st = self.struct()
+        L.check(L.lib().fc_state_rebase(C.byref(self.grid), C.byref(st), L.stream_ptr(stream)),
+                "fc_state_rebase")
+        self._set_base(self.t)
 
     def run(self, land: DeviceLandscape, nsteps: int, *, attach: Optional[Sequence[bool]] = None,
             rng: str = "splitmix", draws: Optional[torch.Tensor] = None, skip_inactive: bool = True,
@@ -341,6 +361,23 @@ class FireBatch:
             raise ValueError(f"state shape {(self.h, self.w)} != landscape {land.shape}")
         if self.t + nsteps > self.max_steps:
             raise ValueError(f"run past max_steps={self.max_steps}")
+        if self.t + nsteps - self.t_base > self.REBASE_SPAN:
+            # beyond the int16 ignition-step range: advance in spans, moving
+            # the base forward between them (the launch parity carries over)
+            while nsteps > 0:
+                room = self.t_base + self.REBASE_SPAN - self.t
+                if room <= 0:
+                    self.rebase(stream)
+                    continue
+                n = min(nsteps, room)
+                self.run(land, n, attach=None if attach is None else list(attach)[:n], rng=rng,
+                         draws=None if draws is None else draws[:n],
+                         skip_inactive=skip_inactive, window=window,
+                         wind_schedule=wind_schedule, shard=shard, stream=stream)
+                attach = None if attach is None else list(attach)[n:]
+                draws = None if draws is None else draws[n:]
+                nsteps -= n
+            return
         att = None
         if attach is not None:
             att_np = np.ascontiguousarray(np.asarray(attach, dtype=np.uint8)[:nsteps])
@@ -560,6 +597,8 @@ class FireBatch:
             mstride = 0
         else:
             mstride = self._hw
+        if any(int(s) < self.t_base for s in obs_steps):
+            raise ValueError(f"observation steps before the last rebase (t_base={self.t_base})")
         obs = (C.c_int32 * S)(*[int(s) for s in obs_steps])
         loss = torch.empty((self.m, 2 + 2 * S), dtype=torch.float64, device=self.device)
         crop = torch.empty((self.m, S, 4), dtype=torch.int32, device=self.device)

@@ -297,41 +297,44 @@ def run_simulation(land: Landscape, params: ModelParams, init, steps: int, seed:
     cuts |= {u.apply_at_step for u in schedule}
     if snapshot_every:
         cuts |= {s + 1 for s in range(snapshot_every, steps + 1, snapshot_every)}
+    # runs beyond the int16 ignition-step span rebase between segments
+    span = FireBatch.REBASE_SPAN
+    cuts |= set(range(span + 1, steps + 1, span))
     cuts = sorted(c for c in cuts if 1 <= c <= steps + 1)
+    if attach_set and steps > span and min(attach_set) <= ((steps - 1) // span) * span:
+        raise ValueError(f"attached steps must lie in the last {span} steps of a longer run")
     pending = list(schedule)
     vw_now = land.wind_speed
     segments = []      # (t_lo, t_hi, landscape, params8, wind speed) per run segment
-    snap_planes = []
+    # p_ignite of every ignition (and J of the attached ones) in fp64, per
+    # segment as it completes (fc_recompute64 from the live-slot masks)
+    acc64 = torch.as_tensor(state0.accumulator, device=batch.device).reshape(1, *land.shape)
+    acc64 = acc64.contiguous()
+    jac64 = (torch.zeros((1, *land.shape, 4), dtype=torch.float64, device=batch.device)
+             if attach_set else None)
+    snapshots: List[Tuple[int, FireState]] = []
     for a, b in zip(cuts[:-1], cuts[1:]):
         while pending and pending[0].apply_at_step == a:
             upd = pending.pop(0)
             dl = dl.with_wind(upd.wind_speed, upd.wind_direction)
             vw_now = upd.wind_speed
+        if batch.t + (b - a) - batch.t_base > span:
+            batch.rebase()
         seg_draws = None
         if draws is not None:
             seg_draws = draws[a - 1:b - 1]
         batch.run(dl, b - a, rng=rng, draws=seg_draws)
+        batch.recompute64(dl, a - 1, b - 1, acc64, jac64)
         segments.append((a - 1, b - 1, dl, p8, vw_now))
         if snapshot_every and (b - 1) % snapshot_every == 0 and b - 1 >= 1:
-            bu, bd = batch.unpack()
-            snap_planes.append((b - 1, bu[0].bool().cpu().numpy(), bd[0].bool().cpu().numpy()))
-    # p_ignite of every ignition (and J of the attached ones) in fp64
-    acc64 = torch.as_tensor(state0.accumulator, device=batch.device).reshape(1, *land.shape)
-    acc64 = acc64.contiguous()
-    jac64 = (torch.zeros((1, *land.shape, 4), dtype=torch.float64, device=batch.device)
-             if attach_set else None)
-    for t_lo, t_hi, dl_seg, _, _ in segments:
-        batch.recompute64(dl_seg, t_lo, t_hi, acc64, jac64)
+            st = FireState(np.zeros(land.shape, bool), np.zeros(land.shape, bool),
+                           acc64[0].cpu().numpy(), b - 1)
+            _pull_planes(batch, st)
+            snapshots.append((b - 1, st))
     final = FireState(np.zeros(land.shape, bool), np.zeros(land.shape, bool), np.zeros(land.shape),
                       steps)
     _pull_planes(batch, final)
     final.accumulator[...] = acc64[0].cpu().numpy()
-    snapshots: List[Tuple[int, FireState]] = []
-    if snap_planes:
-        t_ign = batch.t_ign[0].cpu().numpy()
-        for s_, bu, bd in snap_planes:
-            acc_s = np.where(t_ign < s_, final.accumulator, 0.0)
-            snapshots.append((s_, FireState(bu, bd, acc_s, s_)))
     ser = batch.series()[0] if steps > 0 else np.zeros((0, 2), np.int64)
     series = [StepStats(t=i + 1, burning=int(ser[i, 0]), burned=int(ser[i, 1]))
               for i in range(steps)]

@@ -123,7 +123,8 @@ class RunBinding:
                 fields_cache.clear()
                 fields_cache[key] = build_fields_device(seg[2], seg[3], with_gradients=True)
             F = fields_cache[key]
-            idx = torch.nonzero(t_ign == t)  # row-major, as np.nonzero (kernel.py:345-347)
+            # t_ign counts from the batch's base; row-major, as np.nonzero (kernel.py:345-347)
+            idx = torch.nonzero(t_ign == t - self.batch.t_base)
             rows, cols = idx[:, 0], idx[:, 1]
             n = rows.numel()
             bits = live[rows, cols].to(torch.int32)

@@ -315,3 +315,40 @@ def test_member_sharding_is_partition_invariant(rng):
         # without the offset the second shard would replay members 0..2's draws
         wrong = run(shard_members(M, 1, 2), 0)
         assert not torch.equal(wrong[0], parts[1][0])
+
+
+def test_run_longer_than_int16_ignition_steps():
+    """kernel.py:453-468 has no step limit: a 70,000-step run (two rebases of
+    the int16 ignition-step base) keeps equal to the oracle -- a slow fire
+    (cells keep burning, (1+canopy)(1+density) = 1e-4, no wind, flat) that
+    still ignites cells after step 60,000."""
+    n, steps = 48, 70000
+    z = np.zeros((n, n))
+    dl = F.DeviceLandscape.from_elevation(z, z, z, z - 0.99, z - 0.99)
+    pr = (0.0, 0.0, 0.0, 0.2, 1.0)
+    b = F.FireBatch((n, n), 1, max_steps=steps)
+    b.set_params(F.pack_params(*pr))
+    b.set_seeds([5])
+    init = np.zeros((n, n), bool)
+    init[0, :] = True
+    b.reset(init)
+    b.run(dl, steps, window=16)
+    assert b.t_base >= 60000
+    arr = dict(wind_speed=z, wind_direction=z, slope=np.zeros((n, n, 3, 3)), canopy=z - 0.99,
+               density=z - 0.99)
+    res = O.run(**arr, params=P(pr), init=init, steps=steps, seed=5, threads=THREADS)
+    bu, bd = (x[0].bool().cpu().numpy() for x in b.unpack())
+    assert np.array_equal(bu, res.burning) and np.array_equal(bd, res.burned)
+    np.testing.assert_allclose(b.acc[0].double().cpu().numpy(), res.acc, rtol=RTOL_ACC)
+    assert np.array_equal(b.series()[0], res.series)
+    late = res.t_ign[(res.t_ign >= b.t_base) & (res.t_ign < steps)]
+    assert late.size > 0  # ignitions after the last rebase
+    tig = b.t_ign[0].cpu().numpy().astype(np.int64)
+    after = (res.t_ign >= b.t_base) & (res.t_ign < steps)
+    assert np.array_equal(tig[after] + b.t_base, res.t_ign[after])
+    # the reference-signature API runs it too (fp64 accumulator)
+    sim = F.run_simulation(F.Landscape(**arr), F.ModelParams(c1=0.0, c2=0.0, a=0.0, p_h=0.2,
+                                                            p_continue=1.0),
+                           init, steps, 5)
+    assert np.array_equal(sim.state.burning, res.burning)
+    np.testing.assert_allclose(sim.state.accumulator, res.acc, rtol=1e-10)
