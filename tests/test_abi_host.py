@@ -165,3 +165,33 @@ def test_pyrocell_alias_exposes_the_reference_api():
         sys.path.remove(alias)
         for k in [k for k in sys.modules if k == "pyrocell" or k.startswith("pyrocell.")]:
             del sys.modules[k]
+
+
+def _header_arity():
+    hdr = open(_lib.HEADER).read()
+    hdr = re.sub(r"/\*.*?\*/", "", hdr, flags=re.S)
+    out = {}
+    for name, args in re.findall(r"\b(fc_[a-z_0-9]+)\s*\(([^)]*)\)\s*;", hdr):
+        args = args.strip()
+        out[name] = 0 if args in ("", "void") else args.count(",") + 1
+    return out
+
+
+def test_binding_and_integration_stub_match_header_arity():
+    """Every ctypes signature (_lib) and every call in the INTEGRATION.md stub
+    (tools/pyrocell_firecell_stub.py) passes exactly as many arguments as the
+    header declares (the r1 stub passed 14 of fc_run's 16)."""
+    import ast
+    arity = _header_arity()
+    L = _lib.lib()
+    for name, n in arity.items():
+        assert len(getattr(L, name).argtypes) == n, name
+    src = open(os.path.join(REPO, "tools", "pyrocell_firecell_stub.py")).read()
+    calls = [n for n in ast.walk(ast.parse(src)) if isinstance(n, ast.Call)
+             and isinstance(n.func, ast.Attribute) and n.func.attr.startswith("fc_")]
+    assert {c.func.attr for c in calls} == {"fc_run", "fc_contract"}
+    for c in calls:
+        assert len(c.args) == arity[c.func.attr], c.func.attr
+    doc = open(os.path.join(REPO, "INTEGRATION.md")).read()
+    body = src[src.index("def run_device"):src.index("def contract_device")].strip()
+    assert body in doc, "INTEGRATION.md must show the stub that the tests run"

@@ -1102,3 +1102,33 @@ def test_ensemble_runner_refilled_pinned_inputs():
         b.run(dl, steps)
         np.testing.assert_array_equal(bu_h, b.unpack()[0].cpu().numpy())
         np.testing.assert_array_equal(acc_h, b.acc.cpu().numpy())
+
+
+def test_integration_stub_runs_the_device_path():
+    """The maintainer-side ctypes stub INTEGRATION.md shows
+    (tools/pyrocell_firecell_stub.py), executed: same bytes as FireBatch.run
+    and the same gradient as FireBatch.contract."""
+    import importlib.util
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools",
+                        "pyrocell_firecell_stub.py")
+    spec = importlib.util.spec_from_file_location("pyrocell_firecell_stub", path)
+    stub = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(stub)
+    n, steps = 96, 40
+    env = S.make_environment(n, seed=13)
+    dl = F.DeviceLandscape.from_environment(env)
+    runs = []
+    for via_stub in (True, False):
+        b = F.FireBatch((n, n), 1, max_steps=steps, with_jacobian=True)
+        b.set_params(F.pack_params(0.05, 0.12, 0.08, 0.6, 0.4))
+        b.set_seeds([9])
+        b.reset(S.center_ignition(n))
+        if via_stub:
+            stub.run_device(b, dl, steps, [1] * steps)
+        else:
+            b.run(dl, steps, attach=[True] * steps, window=8)
+        g = torch.as_tensor(np.random.default_rng(1).standard_normal((1, n, n)))
+        grad = stub.contract_device(b, g) if via_stub else b.contract(g)
+        runs.append((b.planes.clone(), b.acc.clone(), grad))
+    assert torch.equal(runs[0][0], runs[1][0]) and torch.equal(runs[0][1], runs[1][1])
+    assert torch.equal(runs[0][2], runs[1][2])
