@@ -852,6 +852,11 @@ def spawn_ranks(args) -> bool:
 def main():
     args = parse()
     spawn_ranks(args)
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        # NCCL's INFO log (rings, channels, P2P over NVLink) on stderr, so the
+        # run shows the N ranks it used; stdout keeps the one JSON line
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     if args.impl == "reference":
         run_reference(args)
     else:
