@@ -124,6 +124,11 @@ typedef struct {
     uint8_t* live;          /* [M][H][W] bit k = slot k's neighbour burned pre-step, written
                                at every ignition (the tape mask of kernel.py:380-383); read
                                only where t_ign marks an ignition.  May be NULL. */
+    void* sched;            /* fc_sched_workspace_bytes(g, max_steps) bytes, or NULL: with it,
+                               an ensemble (M >= 2, keyed SplitMix draws, activity lists,
+                               4- or 8-step windows) runs each fc_run call as one persistent
+                               dataflow launch in which every member advances window by
+                               window on its own (same bytes as one launch per window) */
     int32_t max_steps;
     int32_t t_base;         /* t_ign and tile_first hold (pre-step index - t_base): int16
                                t_ign spans 32766 steps from the base, and runs longer than
@@ -148,6 +153,7 @@ typedef struct {
 void fc_grid_make(int32_t height, int32_t width, int32_t members, fc_grid* out);
 size_t fc_plane_words(const fc_grid* g);              /* uint32 words per plane   */
 size_t fc_loss_workspace_bytes(const fc_grid* g, int32_t n_targets);
+size_t fc_sched_workspace_bytes(const fc_grid* g, int32_t max_steps);  /* fc_state.sched */
 
 /* -------------------------------------------------------------- state --- */
 /* new_fire_state (model.py:180-200) for every member: init is uint8 [M][H][W]

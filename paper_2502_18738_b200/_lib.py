@@ -29,7 +29,8 @@ NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", 
               "-Xcompiler", "-fPIC", "-shared"]
 
 # Every symbol include/firecell.h declares (checked by the CPU test suite).
-EXPORTS = ("fc_grid_make", "fc_plane_words", "fc_loss_workspace_bytes", "fc_state_init",
+EXPORTS = ("fc_grid_make", "fc_plane_words", "fc_loss_workspace_bytes", "fc_sched_workspace_bytes",
+           "fc_state_init",
            "fc_state_reset",
            "fc_state_unpack", "fc_state_export", "fc_state_rebase", "fc_host_device_pointer", "fc_inject", "fc_run", "fc_run_pass", "fc_mark_ghosts", "fc_activity_scan",
            "fc_contract", "fc_recompute64", "fc_contract_steps", "fc_loss_grad",
@@ -62,7 +63,7 @@ class FcState(C.Structure):
                 ("acc", C.c_void_p), ("t_ign", C.c_void_p), ("jac", C.c_void_p),
                 ("flags", C.c_void_p), ("counters", C.c_void_p), ("tile_list", C.c_void_p),
                 ("list_count", C.c_void_p), ("tile_fire", C.c_void_p), ("tile_first", C.c_void_p),
-                ("live", C.c_void_p), ("max_steps", C.c_int32),
+                ("live", C.c_void_p), ("sched", C.c_void_p), ("max_steps", C.c_int32),
                 ("t_base", C.c_int32)]
 
 
@@ -101,6 +102,7 @@ def lib():
             "fc_grid_make": (None, [i32, i32, i32, G]),
             "fc_plane_words": (C.c_size_t, [G]),
             "fc_loss_workspace_bytes": (C.c_size_t, [G, i32]),
+            "fc_sched_workspace_bytes": (C.c_size_t, [G, i32]),
             "fc_state_init": (C.c_int, [G, ST, vp, i64, i32, vp]),
             "fc_state_reset": (C.c_int, [G, ST, vp, i64, i32, vp]),
             "fc_state_unpack": (C.c_int, [G, ST, i32, vp, vp, vp]),

@@ -203,11 +203,14 @@ class FireBatch:
 
     def __init__(self, shape, members: int = 1, *, max_steps: int = 1024,
                  with_jacobian: bool = False, member0: int = 0, record_live: bool = False,
-                 device=None):
+                 dataflow: bool = True, device=None):
         """member0: global index of local member 0 when an ensemble is
         sharded over ranks (the member word of the Philox counter).
         record_live: keep each ignition's live-slot mask (1 B per cell), which
-        recompute64() turns into fp64 accumulators and Jacobians."""
+        recompute64() turns into fp64 accumulators and Jacobians.
+        dataflow: ensembles (members >= 2) run each run() call as one
+        persistent launch in which members advance independently
+        (fc_state.sched); False keeps one launch per window."""
         L.require_cuda()
         dev = _dev(device)
         self.device = dev
@@ -248,6 +251,11 @@ class FireBatch:
         self._status = torch.zeros((self.m,), dtype=torch.int32, device=dev)
         ws = max(L.lib().fc_loss_workspace_bytes(C.byref(self.grid), 8), 1 << 12)
         self.workspace = torch.empty((ws,), dtype=torch.uint8, device=dev)
+        # ensembles: the dataflow scheduler's workspace (fc_state.sched)
+        self.sched = (torch.empty((L.lib().fc_sched_workspace_bytes(C.byref(self.grid),
+                                                                    self.max_steps),),
+                                  dtype=torch.uint8, device=dev)
+                      if self.m >= 2 and dataflow else None)
         self.t = 0
         self.t_base = 0  # t_ign / tile_first count steps from here (fc_state.t_base)
         self.q = 0  # launches since reset (burning-buffer parity, activity lists)
@@ -274,6 +282,7 @@ class FireBatch:
         s.tile_fire = L.ptr(self.tile_fire)
         s.tile_first = L.ptr(self.tile_first)
         s.live = L.ptr(self.live)
+        s.sched = L.ptr(self.sched)
         s.max_steps = self.max_steps
         s.t_base = self.t_base
         self._struct = s

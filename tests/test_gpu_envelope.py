@@ -352,3 +352,46 @@ def test_run_longer_than_int16_ignition_steps():
                            init, steps, 5)
     assert np.array_equal(sim.state.burning, res.burning)
     np.testing.assert_allclose(sim.state.accumulator, res.acc, rtol=1e-10)
+
+
+@pytest.mark.parametrize("window,attach,wind,tensor", [(8, False, False, False),
+                                                        (4, True, True, False),
+                                                        (8, True, False, True)])
+def test_dataflow_ensemble_equals_one_launch_per_window(window, attach, wind, tensor):
+    """The dataflow mode (one persistent launch per fc_run call, members
+    advancing window by window on their own) gives the same bytes as one
+    launch per window: planes, accumulator, ignition steps, Jacobians,
+    per-step counters, tile_first -- also across a split run."""
+    from paper_2502_18738_b200.device import wind_ramp_schedule
+    n, steps, M = 384, 150, 6
+    env = S.make_environment(n, seed=41)
+    if tensor:
+        arr = S.reference_landscape_arrays(env, O.slope_from_altitude)
+        dl = F.DeviceLandscape.from_slope_tensor(arr["wind_speed"], arr["wind_direction"],
+                                                 arr["slope"], arr["canopy"], arr["density"])
+    else:
+        dl = F.DeviceLandscape.from_environment(env)
+    sched = wind_ramp_schedule(steps, 2.0, 12.0, 90.0) if wind else None
+    params = np.array([F.pack_params(0.05, 0.12, 0.08, p, 0.4) for p in S.ensemble_ph(M)])
+    init = S.center_ignition(n)
+    att = [attach and (s % 3 != 2) for s in range(steps)]
+    out = []
+    for df in (False, True):
+        b = F.FireBatch((n, n), M, max_steps=steps, with_jacobian=attach, dataflow=df)
+        assert (b.sched is not None) == df
+        b.set_params(params)
+        b.set_seeds(list(range(10, 10 + M)))
+        b.reset(init)
+        b.run(dl, 70, attach=att[:70], window=window, wind_schedule=sched)
+        b.run(dl, steps - 70, attach=att[70:], window=window, wind_schedule=sched)
+        out.append((b.planes.clone(), b.acc.clone(), b.t_ign.clone(),
+                    None if b.jac is None else b.jac.clone(), b.counters.clone(),
+                    b.tile_first.clone(), b.q, b.list_count[:2 * (steps + 3) + 1].clone()))
+    a, d = out
+    assert int(a[0].count_nonzero()) > 1000
+    for k in range(6):
+        if a[k] is not None:
+            assert torch.equal(a[k], d[k]), k
+    assert a[6] == d[6]
+    q = a[6]
+    assert torch.equal(a[7][q:q + 2], d[7][q:q + 2])  # the next launches' list lengths
