@@ -16,11 +16,21 @@ from paper_2502_18738_b200 import _lib as L, synthetic as S  # noqa: E402
 
 def main():
     n = 16384
-    b = F.FireBatch((n, n), 1, max_steps=8)
-    b.reset(S.random_blocks(n, n, 8, 5, seed=3))
-    st = b.struct()
-    scan = lambda: L.check(L.lib().fc_activity_scan(C.byref(b.grid), C.byref(st), 0,
-                                                    L.stream_ptr()), "scan")
+    # four states scanned in turn: each scan's 67 MB of plane traffic is
+    # evicted from the 126 MB L2 by the next three before it comes round
+    bs = []
+    for k in range(4):
+        b = F.FireBatch((n, n), 1, max_steps=8)
+        b.reset(S.random_blocks(n, n, 8, 5, seed=3 + k))
+        bs.append((b, b.struct()))
+    b, st = bs[0]
+    it = [0]
+
+    def scan():
+        bb, ss = bs[it[0] % 4]
+        it[0] += 1
+        L.check(L.lib().fc_activity_scan(C.byref(bb.grid), C.byref(ss), 0, L.stream_ptr()),
+                "scan")
     ts = []
     for _ in range(30):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
