@@ -431,7 +431,7 @@ def run_ours(args):
             clk = 1.965e9
             floor_us = inst / (148 * 4 * clk) * 1e6  # 4 issue slots per SM per clock
             roofline["issue_roofline"] = {
-                "warp_instructions_per_launch": inst, "issue_floor_us": floor_us,
+                "warp_instructions_per_window": inst, "issue_floor_us": floor_us,
                 "frac": floor_us / avg_us,
                 "note": "148 SMs x 4 schedulers x 1 warp-instruction/clock at 1965 MHz; the "
                         "kernel is latency-bound (barrier and memory-latency stalls), "
@@ -704,12 +704,15 @@ def bench_row_sharded(dev, rank, world, steps=1000, windows=(1, 4, 8)):
             # host work (~0.1 ms per window in Python) would otherwise bound
             # the k = 1 schedule
             mode = "cuda-graph"
-            try:
-                graph = F.CapturedSequence(one)
-                run = graph.replay
-            except Exception as exc:  # fall back to eager launches, say so
-                torch.cuda.synchronize()
-                mode, run = f"eager (capture failed: {type(exc).__name__})", one
+            if os.environ.get("FC_SHARD_GRAPH", "1") == "0":
+                mode, run = "eager (FC_SHARD_GRAPH=0)", one
+            else:
+                try:
+                    graph = F.CapturedSequence(one)
+                    run = graph.replay
+                except Exception as exc:  # fall back to eager launches, say so
+                    torch.cuda.synchronize()
+                    mode, run = f"eager (capture failed: {type(exc).__name__})", one
             barrier()
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -395,3 +395,28 @@ def test_dataflow_ensemble_equals_one_launch_per_window(window, attach, wind, te
     assert a[6] == d[6]
     q = a[6]
     assert torch.equal(a[7][q:q + 2], d[7][q:q + 2])  # the next launches' list lengths
+
+
+def test_dataflow_many_members_injection_and_window_change():
+    """Dataflow with 64 members of very different fire sizes (p_h from 0.2 to
+    1), an injection between runs and the window growing from 4 to 8 (the
+    lists are re-marked, split and merged around every call): the same bytes
+    as one launch per window."""
+    n, M = 160, 64
+    env = S.make_environment(n, seed=43)
+    dl = F.DeviceLandscape.from_environment(env)
+    params = np.array([F.pack_params(0.05, 0.12, 0.08, 0.2 + 0.8 * m / (M - 1), 0.5)
+                       for m in range(M)])
+    init = S.center_ignition(n)
+    out = []
+    for df in (False, True):
+        b = F.FireBatch((n, n), M, max_steps=90, dataflow=df)
+        b.set_params(params)
+        b.set_seeds(list(range(M)))
+        b.reset(init)
+        b.run(dl, 30, window=4)
+        b.inject([(m, 10, 10 + m) for m in range(0, M, 3)])
+        b.run(dl, 60, window=8)
+        out.append((b.planes.clone(), b.acc.clone(), b.t_ign.clone(), b.counters.clone()))
+    for k in range(4):
+        assert torch.equal(out[0][k], out[1][k]), k
