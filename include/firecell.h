@@ -38,10 +38,12 @@
  *   activity      flags int32 [M][TY][TX] = last pre-step index at which the
  *                 tile must be visited; tile_list int32 [3][M*TY*TX] rotating
  *                 compacted lists of tiles active at steps t, t+1, t+2 with
- *                 list_count int32 [2 (max_steps+3) + 1] (zeroed by fc_state_init):
- *                 list lengths, per-launch work counters, and last the
- *                 neighbour-activation distance the current lists were built
- *                 with (0 = full 3x3 tile neighbourhoods).
+ *                 list_count int32 [2 (max_steps+3) + 4] (zeroed by fc_state_init,
+ *                 8-byte aligned): list lengths, per-launch work counters,
+ *                 the neighbour-activation distance the current lists were
+ *                 built with (0 = full 3x3 tile neighbourhoods), one unused
+ *                 word, and last the dense scan's (ticket, count) pair, zero
+ *                 between scans.
  *   params        fp64 [M][8] = {c1, c2, a, p_h, p_continue, norm_c, 0, 0}.
  */
 #ifndef FIRECELL_H
@@ -111,9 +113,10 @@ typedef struct {
     int32_t* flags;         /* [M][TY][TX] last pre-step index active   */
     int32_t* counters;      /* [M][max_steps][FC_NCOUNTER]              */
     int32_t* tile_list;     /* [3][M*TY*TX] rotating active-tile lists  */
-    int32_t* list_count;    /* [2 (max_steps+3) + 1]: list length, then work-
-                               distribution counter, of each launch; last the
-                               neighbour-activation distance of the lists */
+    int32_t* list_count;    /* [2 (max_steps+3) + 4]: list length, then work-
+                               distribution counter, of each launch; the
+                               neighbour-activation distance of the lists; pad;
+                               the dense scan's 64-bit (ticket, count) word */
     uint8_t* tile_fire;     /* [M][TY][TX] per-tile work estimate (log2), written by
                                the step kernel; orders ensemble lists (may be NULL) */
     int32_t* tile_first;    /* [M][TY][TX] earliest pre-step index at which a cell of the
@@ -257,7 +260,8 @@ int fc_run_pass(const fc_grid* g, const fc_landscape* land, const fc_state* s,
 /* Dense-sweep activity scan for launch `phase` (the first half of every
  * skip_inactive = 0 launch, exposed for measurement): streams the burning
  * plane, lists every tile with fire in its 3x3 tile neighbourhood and writes
- * the all-zero next state of every other tile (HBM-bound). */
+ * the all-zero next state of every other tile (HBM-bound).  One kernel
+ * launch: the list length is set by the scan's last CTA. */
 int fc_activity_scan(const fc_grid* g, const fc_state* s, int32_t phase, fc_stream_t stream);
 
 /* After the ghost rows were refreshed with the neighbours' state at launch

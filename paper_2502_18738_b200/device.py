@@ -239,7 +239,7 @@ class FireBatch:
         # launches are bounded by steps (>= 1 step per launch) plus resets' lists
         ntiles = self.m * self.grid.tiles_y * self.grid.tiles_x
         self.tile_list = torch.empty((3, ntiles), dtype=torch.int32, device=dev)
-        self.list_count = torch.zeros((2 * (self.max_steps + 3) + 1,), dtype=torch.int32, device=dev)
+        self.list_count = torch.zeros((2 * (self.max_steps + 3) + 4,), dtype=torch.int32, device=dev)
         self.tile_fire = torch.zeros((ntiles,), dtype=torch.uint8, device=dev)
         self.tile_first = torch.full((ntiles,), L.T_NEVER, dtype=torch.int32, device=dev)
         self._cells_clean = False  # acc / t_ign hold no library-written state yet
