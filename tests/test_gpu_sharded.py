@@ -59,3 +59,42 @@ def test_row_sharded_equals_unsharded(world, window, attach):
     assert torch.equal(torch.cat(parts_t), ref.t_ign[0])
     assert np.array_equal(series, ref.series()[0])
     assert int(rb.sum() + rd.sum()) > 500
+
+
+@pytest.mark.parametrize("world,window", [(2, 8), (3, 4)])
+def test_row_sharded_dense_sweep_equals_unsharded(world, window):
+    """Dense sweeps (skip_inactive=False) of row shards, one fc_run per
+    window with the ghost rows refreshed in between: the dense scan lists
+    owned tiles next to ghost-row fire and never writes ghost rows, so the
+    result equals the unsharded run byte for byte."""
+    from paper_2502_18738_b200.sharded import LocalHalo
+    h, w, steps = 300, 140, 60
+    env = S.make_environment(h, w, seed=33)
+    init = S.random_blocks(h, w, 6, 5, seed=4) | S.center_ignition(h, w)
+    params = F.pack_params(0.06, 0.12, 0.08, 0.6, 0.45)
+    ref = F.FireBatch((h, w), 1, max_steps=steps)
+    ref.set_params(params)
+    ref.set_seeds([78])
+    ref.reset(init)
+    ref.run(F.DeviceLandscape.from_environment(env), steps, window=window)
+    rb, rd = ref.unpack()
+    shards = []
+    for r in range(world):
+        sh = RowShard(RowPartition(h, world, r), env.elevation, env.wind_speed,
+                      env.wind_direction, env.canopy, env.density, init, max_steps=steps)
+        sh.batch.set_params(params)
+        sh.batch.set_seeds([78])
+        shards.append(sh)
+    done = 0
+    while done < steps:
+        n = min(window, steps - done)
+        for sh in shards:
+            sh.run_window(n, window, skip_inactive=False)
+        LocalHalo()(shards)
+        done += n
+    got_b = torch.cat([sh.owned(sh.batch.unpack()[0][0]) for sh in shards])
+    got_d = torch.cat([sh.owned(sh.batch.unpack()[1][0]) for sh in shards])
+    assert torch.equal(got_b, rb[0]) and torch.equal(got_d, rd[0])
+    assert torch.equal(torch.cat([sh.owned(sh.batch.acc[0]) for sh in shards]), ref.acc[0])
+    assert torch.equal(torch.cat([sh.owned(sh.batch.t_ign[0]) for sh in shards]), ref.t_ign[0])
+    assert int(rb.sum() + rd.sum()) > 500
