@@ -132,6 +132,9 @@ typedef struct {
                                4- or 8-step windows) runs each fc_run call as one persistent
                                dataflow launch in which every member advances window by
                                window on its own (same bytes as one launch per window) */
+    int64_t* init_burning;  /* [M] burning cells of each member's initial mask, written by
+                               fc_state_init / fc_state_reset (the series' step-0 count,
+                               kernel.py:431-439), or NULL */
     int32_t max_steps;
     int32_t t_base;         /* t_ign and tile_first hold (pre-step index - t_base): int16
                                t_ign spans 32766 steps from the base, and runs longer than

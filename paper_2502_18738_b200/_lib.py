@@ -63,7 +63,8 @@ class FcState(C.Structure):
                 ("acc", C.c_void_p), ("t_ign", C.c_void_p), ("jac", C.c_void_p),
                 ("flags", C.c_void_p), ("counters", C.c_void_p), ("tile_list", C.c_void_p),
                 ("list_count", C.c_void_p), ("tile_fire", C.c_void_p), ("tile_first", C.c_void_p),
-                ("live", C.c_void_p), ("sched", C.c_void_p), ("max_steps", C.c_int32),
+                ("live", C.c_void_p), ("sched", C.c_void_p), ("init_burning", C.c_void_p),
+                ("max_steps", C.c_int32),
                 ("t_base", C.c_int32)]
 
 

@@ -283,6 +283,7 @@ class FireBatch:
         s.tile_first = L.ptr(self.tile_first)
         s.live = L.ptr(self.live)
         s.sched = L.ptr(self.sched)
+        s.init_burning = L.ptr(self._init_burning_dev)
         s.max_steps = self.max_steps
         s.t_base = self.t_base
         self._struct = s
@@ -318,10 +319,9 @@ class FireBatch:
             stride = self._hw
         else:
             raise ValueError(f"initial fire mask must be 2-D or (M,H,W), got {tuple(m8.shape)}")
-        # initial burning counts stay on the device (no host sync inside a
-        # timed or captured sequence); series() reads them when asked
-        cnt = (m8 != 0).reshape(-1, self._hw).sum(1, dtype=torch.int64)
-        self._init_burning_dev.copy_(cnt.expand(self.m) if m8.dim() == 2 else cnt)
+        # the reset kernels count the initial burning cells into
+        # _init_burning_dev (fc_state.init_burning): no host sync inside a
+        # timed or captured sequence; series() reads them when asked
         self._init_mask = m8.contiguous()
         st = self.struct()
         # after the first full initialisation only the tiles that held fire
