@@ -195,3 +195,27 @@ def test_binding_and_integration_stub_match_header_arity():
     doc = open(os.path.join(REPO, "INTEGRATION.md")).read()
     body = src[src.index("def run_device"):src.index("def contract_device")].strip()
     assert body in doc, "INTEGRATION.md must show the stub that the tests run"
+
+
+def _header_struct_fields(name):
+    hdr = re.sub(r"/\*.*?\*/", "", open(_lib.HEADER).read(), flags=re.S)
+    body = re.search(r"typedef struct \{([^}]*)\}\s*" + name + r"\s*;", hdr).group(1)
+    out = []
+    for decl in (d.strip() for d in body.split(";")):
+        if not decl:
+            continue
+        # "type a, b" / "type* p": the first declarator carries the type
+        first, *rest = decl.split(",")
+        out.append(re.findall(r"(\w+)\s*(?:\[[^\]]*\])?\s*$", first)[0])
+        out += [r.strip().lstrip("*").strip() for r in rest]
+    return out
+
+
+@pytest.mark.parametrize("cname,pyname", [("fc_grid", "FcGrid"), ("fc_landscape", "FcLandscape"),
+                                          ("fc_state", "FcState"), ("fc_shard", "FcShard")])
+def test_ctypes_structs_match_header(cname, pyname):
+    """The ctypes mirrors of the ABI structs list the header's fields in the
+    header's order (a field added on one side only shifts every later one)."""
+    want = _header_struct_fields(cname)
+    got = [f[0] for f in getattr(_lib, pyname)._fields_]
+    assert got == want, (cname, got, want)
