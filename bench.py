@@ -663,11 +663,16 @@ def bench_row_sharded(dev, rank, world, steps=1000, windows=(1, 4, 8)):
     import paper_2502_18738_b200 as F
     from paper_2502_18738_b200 import synthetic as S
     from paper_2502_18738_b200.parallel import allreduce_max, barrier
-    from paper_2502_18738_b200.sharded import RowPartition, RowShard, run_sharded
+    from paper_2502_18738_b200.sharded import (RowPartition, RowShard, connect_peers,
+                                               peer_handshake, run_peer, run_sharded)
     out = {"steps": steps, "ranks": world, "scaling": {"strong": "total work fixed",
                                                          "weak": "work per rank fixed"},
-           "halo": "2 bit planes x 1 tile row (32 rows) each way per launch, NCCL P2P on a "
-                   "communication stream overlapped with the next launch's interior pass"}
+           "halo": "2 bit planes x 1 tile row (32 rows) each way per launch"}
+    halo_peer = ("peer: the boundary pass stores its rows into the neighbours' ghost rows "
+                 "(NVLink, CUDA IPC mappings) and counts the launch in their flag words; "
+                 "streams wait on the flags (fc_peer_halo), no collective in the step loop")
+    halo_nccl = ("nccl: NCCL P2P send/recv on a communication stream overlapped with the next "
+                 "launch's interior pass")
     for kind in ("strong", "weak"):
         H, Wd = (16384, 16384) if kind == "strong" else (2048 * world, 16384)
         nfire = 8 if kind == "strong" else 2 * world
@@ -690,8 +695,23 @@ def bench_row_sharded(dev, rank, world, steps=1000, windows=(1, 4, 8)):
         b.set_params(F.pack_params(0.045, 0.131, 0.078, 0.58, 0.3))
         b.set_seeds([3])
         init_local = init if world == 1 else sh.batch._init_mask
+        peer = False
+        if world > 1:
+            # the fused peer-memory halo unless FC_HALO=nccl or its handshake
+            # fails (then NCCL P2P, recorded in the line)
+            if os.environ.get("FC_HALO", "peer") == "peer":
+                err = connect_peers(sh)  # collective; never raises on a mapping failure
+                peer = peer_handshake(sh)
+                if err or not peer:
+                    res["peer_unavailable"] = (err or "handshake: flags did not arrive")[:200]
+            if not peer:
+                sh.shard.peer = None
+            res["halo"] = halo_peer if peer else halo_nccl
         for k in windows:
             def one():
+                if world > 1 and peer:
+                    run_peer([sh], steps, k, reset=True)
+                    return
                 b.reset(init_local)
                 if world == 1:
                     b.run(land, steps, window=k)
@@ -700,6 +720,8 @@ def bench_row_sharded(dev, rank, world, steps=1000, windows=(1, 4, 8)):
             b.reset(init_local)  # warm-up: communicators, caches
             if world == 1:
                 b.run(land, 2 * k, window=k)
+            elif peer:
+                run_peer([sh], 2 * k, k)
             else:
                 run_sharded(sh, 2 * k, k)
             torch.cuda.synchronize()

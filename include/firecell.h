@@ -148,11 +148,35 @@ typedef struct {
  * keyed by the global row = local row + row0.  Member-sharded ensembles
  * (configs 1 and 4): local member m is global member m + member0, the member
  * word of the Philox counter, so a member draws the same numbers on any rank. */
+/* Peer-memory halo of a row shard (NVLink peers, or IPC mappings on one
+ * device): the boundary pass writes its owned boundary tile rows straight
+ * into the neighbours' ghost tile rows, tile by tile as it computes them, and
+ * its last CTA then stores `seq` into the neighbours' flag words -- compute
+ * and halo transfer in one kernel, no collective.  Protocol (every shard
+ * issues the same sequence of events -- resets and boundary passes -- and
+ * numbers them 1, 2, ...): before its event k a shard makes its stream wait
+ * until both of its own flag words are >= k - 1 (fc_stream_wait_geq); a
+ * boundary pass that is event k runs with seq = k; a reset that is event k
+ * is followed by fc_peer_signal(k).  So a shard reads its ghost rows only
+ * after the neighbours wrote them, writes a neighbour's ghost rows only after
+ * the neighbour read the previous ones, and never races a neighbour's reset. */
+typedef struct {
+    uint32_t* up[4];        /* upper neighbour's {burn0, burn1, burned0, burned1}; NULL: none */
+    uint32_t* down[4];      /* lower neighbour's planes; NULL: none                          */
+    int32_t up_tiles_y;     /* the neighbours' local tile rows (ghost rows included)          */
+    int32_t down_tiles_y;
+    int32_t* up_flag;       /* the upper neighbour's word counting this shard's events        */
+    int32_t* down_flag;     /* the lower neighbour's word                                     */
+    int32_t seq;            /* the event number the next boundary pass stores                 */
+    int32_t pad_;
+} fc_peer_halo;
+
 typedef struct {
     int32_t row0;           /* global row of local row 0                    */
     int32_t ghost_top;      /* ghost tile rows at the top (0 or 1)          */
     int32_t ghost_bottom;   /* ghost tile rows at the bottom (0 or 1)       */
     int32_t member0;        /* global index of local member 0               */
+    const fc_peer_halo* peer; /* NULL, or the peer-memory halo (fc_run_pass pass 2) */
 } fc_shard;
 
 /* ------------------------------------------------------------ sizing --- */
@@ -253,12 +277,26 @@ int fc_run(const fc_grid* g, const fc_landscape* land, const fc_state* s,
  *           activity marks), after the ghost rows hold the neighbours'
  *           state of this launch's input; advances *host_phase.
  * Pass 1 then pass 2 of every launch gives the same bytes as fc_run
- * (kernel.py:307-309 partition invariance; draws keyed by global cells). */
+ * (kernel.py:307-309 partition invariance; draws keyed by global cells).
+ * With shard->peer, pass 2 also stores the boundary tile rows of its output
+ * into the neighbours' ghost tile rows (their input of the next launch) and,
+ * when its last CTA is done, stores peer->seq into the neighbours' flag words
+ * (release, system scope; the protocol is at fc_peer_halo). */
 int fc_run_pass(const fc_grid* g, const fc_landscape* land, const fc_state* s,
                 const double* params, const uint64_t* seeds, int32_t rng_mode, int32_t t0,
                 int32_t nsteps, const uint8_t* host_attach, int32_t window,
                 const double* wind_schedule, const fc_shard* shard, int32_t pass,
                 int32_t* host_phase, fc_stream_t stream);
+
+/* Store `value` into the neighbours' flag words of `peer` once the work
+ * queued before it on `stream` is done (release, system scope): the event
+ * signal of a reset in the peer-halo protocol. */
+int fc_peer_signal(const fc_peer_halo* peer, int32_t value, fc_stream_t stream);
+
+/* Make `stream` wait (without a kernel) until the int32 at device address
+ * `flag` is >= value (wrap-around compare; cuStreamWaitValue32 GEQ): the
+ * peer-halo hand-off between row shards. */
+int fc_stream_wait_geq(const int32_t* flag, int32_t value, fc_stream_t stream);
 
 /* Dense-sweep activity scan for launch `phase` (the first half of every
  * skip_inactive = 0 launch, exposed for measurement): streams the burning

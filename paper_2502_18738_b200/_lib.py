@@ -32,7 +32,7 @@ NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", 
 EXPORTS = ("fc_grid_make", "fc_plane_words", "fc_loss_workspace_bytes", "fc_sched_workspace_bytes",
            "fc_state_init",
            "fc_state_reset",
-           "fc_state_unpack", "fc_state_export", "fc_state_rebase", "fc_host_device_pointer", "fc_inject", "fc_run", "fc_run_pass", "fc_mark_ghosts", "fc_activity_scan",
+           "fc_state_unpack", "fc_state_export", "fc_state_rebase", "fc_host_device_pointer", "fc_inject", "fc_run", "fc_run_pass", "fc_mark_ghosts", "fc_peer_signal", "fc_stream_wait_geq", "fc_activity_scan",
            "fc_contract", "fc_recompute64", "fc_contract_steps", "fc_loss_grad",
            "fc_loss_dense", "fc_adamw", "fc_uniform_grid", "fc_epoch_seed", "fc_build_fields",
            "fc_landscape_build", "fc_landscape_build_ctas",
@@ -52,9 +52,15 @@ class FcLandscape(C.Structure):
                 ("slope_sign", C.c_int32), ("factor_source", C.c_int32), ("pad_", C.c_int32)]
 
 
+class FcPeerHalo(C.Structure):
+    _fields_ = [("up", C.c_void_p * 4), ("down", C.c_void_p * 4), ("up_tiles_y", C.c_int32),
+                ("down_tiles_y", C.c_int32), ("up_flag", C.c_void_p), ("down_flag", C.c_void_p),
+                ("seq", C.c_int32), ("pad_", C.c_int32)]
+
+
 class FcShard(C.Structure):
     _fields_ = [("row0", C.c_int32), ("ghost_top", C.c_int32), ("ghost_bottom", C.c_int32),
-                ("member0", C.c_int32)]
+                ("member0", C.c_int32), ("peer", C.c_void_p)]
 
 
 class FcState(C.Structure):
@@ -117,6 +123,8 @@ def lib():
                                       C.POINTER(i32), vp]),
             "fc_mark_ghosts": (C.c_int, [G, ST, SH, i32, vp]),
             "fc_activity_scan": (C.c_int, [G, ST, i32, vp]),
+            "fc_stream_wait_geq": (C.c_int, [vp, i32, vp]),
+            "fc_peer_signal": (C.c_int, [vp, i32, vp]),
             "fc_contract": (C.c_int, [G, ST, vp, i32, vp, vp, vp]),
             "fc_recompute64": (C.c_int, [G, LS, ST, vp, i32, i32, vp, vp, vp, vp]),
             "fc_contract_steps": (C.c_int, [G, ST, vp, vp, vp, i32, vp, vp, vp]),

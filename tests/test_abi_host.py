@@ -212,6 +212,7 @@ def _header_struct_fields(name):
 
 
 @pytest.mark.parametrize("cname,pyname", [("fc_grid", "FcGrid"), ("fc_landscape", "FcLandscape"),
+                                          ("fc_peer_halo", "FcPeerHalo"),
                                           ("fc_state", "FcState"), ("fc_shard", "FcShard")])
 def test_ctypes_structs_match_header(cname, pyname):
     """The ctypes mirrors of the ABI structs list the header's fields in the
