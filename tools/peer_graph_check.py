@@ -1,5 +1,13 @@
-import sys, torch
-sys.path.insert(0, "/root/repo")
+"""Peer-memory halo under CUDA-graph replay: three emulated row shards on
+one GPU (each on its own stream), the run with reset captured once and
+replayed three times; each replay must equal the unsharded run and leave
+every flag word at zero.  python tools/peer_graph_check.py"""
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2502_18738_b200 as F
 from paper_2502_18738_b200 import synthetic as S
 from paper_2502_18738_b200.sharded import RowPartition, RowShard, connect_local_peers, run_peer_local
