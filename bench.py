@@ -747,8 +747,13 @@ def bench_row_sharded(dev, rank, world, steps=1000, windows=(1, 4, 8)):
             e1.record()
             torch.cuda.synchronize()
             ms = allreduce_max(e0.elapsed_time(e1), dev)
-            res[f"k{k}"] = {"ms": ms, "cell_updates_per_s": H * Wd * steps / (ms / 1e3),
-                            "launch": mode}
+            cus = H * Wd * steps / (ms / 1e3)
+            # B(M=1, k) = (16 + 2) / k bytes per cell-update of a dense
+            # sweep; activity skipping legitimately exceeds that ceiling (frac > 1)
+            b_cu = 18.0 / k
+            res[f"k{k}"] = {"ms": ms, "cell_updates_per_s": cus, "launch": mode,
+                            "dense_equivalent_GBps": cus * b_cu / 1e9,
+                            "dense_equivalent_frac": cus * b_cu / 1e9 / load_peaks()[0]}
             del run
             if mode == "cuda-graph":
                 del graph
