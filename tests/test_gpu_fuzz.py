@@ -1,0 +1,19 @@
+"""Randomised parity sweep (tools/fuzz_parity.py): ragged grids, members,
+windows 1/4/8/16, list or dense sweeps, dataflow on or off, attached steps,
+parameters across PARAM_BOUNDS; same bytes as the plain configuration and
+member 0 equal to the oracle.  (Round 2: 3000 of 3000 configurations pass
+with seed 2; the suite runs 80 with a fixed seed.)"""
+import os
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+
+
+def test_random_configurations_match_plain_run_and_oracle():
+    from fuzz_parity import fuzz
+    failed = fuzz(80, 7, log=lambda *a: None)
+    assert not failed, failed[:5]

@@ -1,0 +1,92 @@
+"""Randomised parity sweep (GPU box): random grids (1..260 a side, ragged),
+members, step counts, windows 1/4/8/16, list or dense sweeps, dataflow on or
+off, attached steps, parameters across PARAM_BOUNDS and random ignitions.
+Every configuration must give the same bytes as the plain configuration
+(one step per launch, activity lists, no dataflow), and member 0 must equal
+the CPU oracle (states exact, acc within 1e-5).
+python tools/fuzz_parity.py [cases] [seed]"""
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+import paper_2502_18738_b200 as F  # noqa: E402
+from paper_2502_18738_b200 import synthetic as S  # noqa: E402
+from golden_util import P  # noqa: E402
+from oracle import oracle as O  # noqa: E402
+
+
+def run_dev(dl, h, w, M, steps, params, seeds, init, attach, window, skip, dataflow):
+    b = F.FireBatch((h, w), M, max_steps=steps, with_jacobian=attach, dataflow=dataflow)
+    b.set_params(params)
+    b.set_seeds(seeds)
+    b.reset(init)
+    b.run(dl, steps, attach=[attach] * steps, window=window, skip_inactive=skip)
+    torch.cuda.synchronize()
+    return b
+
+
+def fuzz(cases: int, seed: int, log=print):
+    """Run `cases` random configurations; returns the failing ones."""
+    rng = np.random.default_rng(seed)
+    failed = []
+    for case in range(cases):
+        h, w = int(rng.integers(1, 261)), int(rng.integers(1, 261))
+        M = int(rng.choice([1, 2, 3, 5]))
+        steps = int(rng.integers(1, 51))
+        attach = bool(rng.integers(0, 2))
+        window = int(rng.choice([1, 4, 8, 16]))
+        skip = bool(rng.integers(0, 3))  # 2:1 lists
+        dataflow = bool(rng.integers(0, 2))
+        pv = [float(rng.uniform(0, 1)), float(rng.uniform(0, 1)), float(rng.uniform(0, 1)),
+              float(rng.uniform(0.2, 1)), float(rng.uniform(0, 1))]
+        env = S.make_environment(h, w, seed=int(rng.integers(0, 1 << 30)))
+        dl = F.DeviceLandscape.from_environment(env)
+        init = np.zeros((h, w), dtype=bool)
+        for _ in range(int(rng.integers(1, 6))):
+            r, c = int(rng.integers(0, h)), int(rng.integers(0, w))
+            k = int(rng.integers(1, 6))
+            init[r:r + k, c:c + k] = True
+        seeds = [int(rng.integers(0, 1 << 62)) for _ in range(M)]
+        params = F.pack_params(*pv)
+        cfg = dict(h=h, w=w, M=M, steps=steps, attach=attach, window=window, skip=skip,
+                   dataflow=dataflow, params=[round(v, 4) for v in pv])
+        try:
+            a = run_dev(dl, h, w, M, steps, params, seeds, init, attach, 1, True, False)
+            b = run_dev(dl, h, w, M, steps, params, seeds, init, attach, window, skip, dataflow)
+            # the current state (the planes hold both launch parities; the
+            # final parity depends on the launch count)
+            ua, ub = a.unpack(), b.unpack()
+            same = (torch.equal(ua[0], ub[0]) and torch.equal(ua[1], ub[1]) and
+                    torch.equal(a.acc, b.acc) and
+                    torch.equal(a.t_ign, b.t_ign) and np.array_equal(a.series(), b.series()) and
+                    (not attach or torch.equal(a.jac, b.jac)))
+            arr = S.reference_landscape_arrays(env, O.slope_from_altitude)
+            res = O.run(**arr, params=P(pv), init=init, steps=steps, seed=seeds[0],
+                        attach_steps=range(1, steps + 1) if attach else (), threads=4)
+            bu, bd = (x.bool().cpu().numpy() for x in b.unpack())
+            ok_states = np.array_equal(bu[0], res.burning) and np.array_equal(bd[0], res.burned)
+            acc = b.acc[0].double().cpu().numpy()
+            ok_acc = np.allclose(acc, res.acc, rtol=1e-5, atol=0)
+            ok = same and ok_states and ok_acc
+        except Exception as exc:  # report and continue
+            ok, same, ok_states, ok_acc = False, repr(exc), None, None
+        if not ok:
+            failed.append((case, cfg, same, ok_states, ok_acc))
+            log("FAIL", case, cfg, "same", same, "states", ok_states, "acc", ok_acc)
+    return failed
+
+
+def main():
+    cases = int(sys.argv[1]) if len(sys.argv) > 1 else 100
+    failed = fuzz(cases, int(sys.argv[2]) if len(sys.argv) > 2 else 0)
+    print(f"{cases - len(failed)}/{cases} configurations pass")
+    return 1 if failed else 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())
