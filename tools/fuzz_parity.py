@@ -20,12 +20,14 @@ from golden_util import P  # noqa: E402
 from oracle import oracle as O  # noqa: E402
 
 
-def run_dev(dl, h, w, M, steps, params, seeds, init, attach, window, skip, dataflow):
+def run_dev(dl, h, w, M, steps, params, seeds, init, attach, window, skip, dataflow, rng="splitmix",
+            wind=None):
     b = F.FireBatch((h, w), M, max_steps=steps, with_jacobian=attach, dataflow=dataflow)
     b.set_params(params)
     b.set_seeds(seeds)
     b.reset(init)
-    b.run(dl, steps, attach=[attach] * steps, window=window, skip_inactive=skip)
+    b.run(dl, steps, attach=[attach] * steps, window=window, skip_inactive=skip, rng=rng,
+          wind_schedule=wind)
     torch.cuda.synchronize()
     return b
 
@@ -53,11 +55,22 @@ def fuzz(cases: int, seed: int, log=print):
             init[r:r + k, c:c + k] = True
         seeds = [int(rng.integers(0, 1 << 62)) for _ in range(M)]
         params = F.pack_params(*pv)
+        draw_rng = "philox" if rng.integers(0, 4) == 0 else "splitmix"
+        wind = None
+        if rng.integers(0, 3) == 0:  # per-step {alpha, beta, gamma} wind schedule
+            wind = np.zeros((steps, 4))
+            wind[:, 0] = rng.uniform(0.5, 1.5, steps)
+            wind[:, 1] = rng.uniform(-2.0, 2.0, steps)
+            wind[:, 2] = rng.uniform(-90.0, 90.0, steps)
+        wind_dev = None if wind is None else torch.as_tensor(wind, device="cuda")
         cfg = dict(h=h, w=w, M=M, steps=steps, attach=attach, window=window, skip=skip,
-                   dataflow=dataflow, params=[round(v, 4) for v in pv])
+                   dataflow=dataflow, rng=draw_rng, wind=wind is not None,
+                   params=[round(v, 4) for v in pv])
         try:
-            a = run_dev(dl, h, w, M, steps, params, seeds, init, attach, 1, True, False)
-            b = run_dev(dl, h, w, M, steps, params, seeds, init, attach, window, skip, dataflow)
+            a = run_dev(dl, h, w, M, steps, params, seeds, init, attach, 1, True, False, draw_rng,
+                        wind_dev)
+            b = run_dev(dl, h, w, M, steps, params, seeds, init, attach, window, skip, dataflow,
+                        draw_rng, wind_dev)
             # the current state (the planes hold both launch parities; the
             # final parity depends on the launch count)
             ua, ub = a.unpack(), b.unpack()
@@ -65,13 +78,16 @@ def fuzz(cases: int, seed: int, log=print):
                     torch.equal(a.acc, b.acc) and
                     torch.equal(a.t_ign, b.t_ign) and np.array_equal(a.series(), b.series()) and
                     (not attach or torch.equal(a.jac, b.jac)))
-            arr = S.reference_landscape_arrays(env, O.slope_from_altitude)
-            res = O.run(**arr, params=P(pv), init=init, steps=steps, seed=seeds[0],
-                        attach_steps=range(1, steps + 1) if attach else (), threads=4)
-            bu, bd = (x.bool().cpu().numpy() for x in b.unpack())
-            ok_states = np.array_equal(bu[0], res.burning) and np.array_equal(bd[0], res.burned)
-            acc = b.acc[0].double().cpu().numpy()
-            ok_acc = np.allclose(acc, res.acc, rtol=1e-5, atol=0)
+            ok_states = ok_acc = True
+            if draw_rng == "splitmix":  # the oracle restates the reference's keyed draws
+                arr = S.reference_landscape_arrays(env, O.slope_from_altitude)
+                res = O.run(**arr, params=P(pv), init=init, steps=steps, seed=seeds[0],
+                            attach_steps=range(1, steps + 1) if attach else (), threads=4,
+                            wind_params=wind)
+                bu, bd = (x.bool().cpu().numpy() for x in b.unpack())
+                ok_states = np.array_equal(bu[0], res.burning) and np.array_equal(bd[0], res.burned)
+                acc = b.acc[0].double().cpu().numpy()
+                ok_acc = np.allclose(acc, res.acc, rtol=1e-5, atol=0)
             ok = same and ok_states and ok_acc
         except Exception as exc:  # report and continue
             ok, same, ok_states, ok_acc = False, repr(exc), None, None
