@@ -32,6 +32,32 @@ def run_dev(dl, h, w, M, steps, params, seeds, init, attach, window, skip, dataf
     return b
 
 
+def check_loss(rng, b, res, h, w, steps):
+    """fc_loss_grad over 1-4 random observation steps and shared random
+    targets against the oracle (combined_loss per step, tape contraction):
+    loss within 1e-5; gradient within 1e-5 of its terms' scale plus the
+    fp32 Jacobian error model (tests/test_gpu_envelope.py)."""
+    S_ = int(rng.integers(1, 5))
+    obs = sorted(set(int(v) for v in rng.integers(1, steps + 1, S_)))
+    targets = []
+    for _ in obs:
+        t = rng.random((h, w)) < rng.uniform(0.0, 0.3)
+        r, c = int(rng.integers(0, h)), int(rng.integers(0, w))
+        t[r:r + int(rng.integers(1, 40)), c:c + int(rng.integers(1, 40))] = True
+        targets.append(t)
+    loss, _, grad, _ = b.loss_grad(torch.as_tensor(np.stack(targets)), obs)
+    total, g_ref = O.multi_target_grad(res, obs, targets)
+    g_cell = np.zeros((h, w))
+    for s_, tgt in zip(obs, targets):
+        acc_s = np.where(res.t_ign < s_, res.acc, 0.0)
+        g_cell += np.where(res.t_ign < s_, O.combined_loss(acc_s, tgt)[3], 0.0)
+    scale = O.contract(1e-5 * res.jac_abs + res.jac_floor + res.jac_cond, np.abs(g_cell))
+    got = grad[0].cpu().numpy() * float(os.environ.get("FUZZ_GRAD_SCALE", "1"))  # sanity: 1.0001 must fail
+    ok_l = abs(float(loss[0, 0]) - total) <= 1e-5 * abs(total) + 1e-12
+    ok_g = bool(np.all(np.abs(got - g_ref) <= scale + 1e-5 * np.abs(g_ref) + 1e-300))
+    return ok_l and ok_g
+
+
 def fuzz(cases: int, seed: int, log=print):
     """Run `cases` random configurations; returns the failing ones."""
     rng = np.random.default_rng(seed)
@@ -78,17 +104,21 @@ def fuzz(cases: int, seed: int, log=print):
                     torch.equal(a.acc, b.acc) and
                     torch.equal(a.t_ign, b.t_ign) and np.array_equal(a.series(), b.series()) and
                     (not attach or torch.equal(a.jac, b.jac)))
-            ok_states = ok_acc = True
+            ok_states = ok_acc = ok_loss = True
             if draw_rng == "splitmix":  # the oracle restates the reference's keyed draws
                 arr = S.reference_landscape_arrays(env, O.slope_from_altitude)
                 res = O.run(**arr, params=P(pv), init=init, steps=steps, seed=seeds[0],
                             attach_steps=range(1, steps + 1) if attach else (), threads=4,
-                            wind_params=wind)
+                            wind_params=wind, want_jac_abs=attach)
                 bu, bd = (x.bool().cpu().numpy() for x in b.unpack())
                 ok_states = np.array_equal(bu[0], res.burning) and np.array_equal(bd[0], res.burned)
                 acc = b.acc[0].double().cpu().numpy()
                 ok_acc = np.allclose(acc, res.acc, rtol=1e-5, atol=0)
-            ok = same and ok_states and ok_acc
+                if attach:
+                    ok_loss = check_loss(rng, b, res, h, w, steps)
+            ok = same and ok_states and ok_acc and ok_loss
+            if not ok_loss:
+                same = f"{same} (loss/gradient off)"
         except Exception as exc:  # report and continue
             ok, same, ok_states, ok_acc = False, repr(exc), None, None
         if not ok:
