@@ -18,3 +18,9 @@ def test_random_configurations_match_plain_run_and_oracle():
     from fuzz_parity import fuzz
     failed = fuzz(80, 7, log=lambda *a: None)
     assert not failed, failed[:5]
+
+
+def test_random_row_shards_match_unsharded():
+    from fuzz_parity import fuzz_shards
+    failed = fuzz_shards(12, 7, log=lambda *a: None)
+    assert not failed, failed[:5]

@@ -127,11 +127,76 @@ def fuzz(cases: int, seed: int, log=print):
     return failed
 
 
+def fuzz_shards(cases: int, seed: int, log=print):
+    """Row shards (2-5 emulated on one GPU, each on its own stream) with the
+    peer-memory halo or the exchange schedule, random heights/widths,
+    windows, attached steps and dense or list sweeps: the owned rows must
+    equal the unsharded run."""
+    from paper_2502_18738_b200.sharded import (RowPartition, RowShard, connect_local_peers,
+                                               run_peer_local, run_sharded_local)
+    rng = np.random.default_rng(seed)
+    failed = []
+    for case in range(cases):
+        world = int(rng.integers(2, 6))
+        h = int(rng.integers(32 * world, 32 * world + 200))
+        w = int(rng.integers(1, 200))
+        steps = int(rng.integers(1, 60))
+        window = int(rng.choice([1, 4, 8, 16]))
+        attach = bool(rng.integers(0, 2))
+        peer = bool(rng.integers(0, 2))
+        env = S.make_environment(h, w, seed=int(rng.integers(0, 1 << 30)))
+        init = np.zeros((h, w), dtype=bool)
+        for _ in range(int(rng.integers(1, 8))):
+            r, c = int(rng.integers(0, h)), int(rng.integers(0, w))
+            init[r:r + 4, c:c + 4] = True
+        pv = [float(rng.uniform(0, 1)), float(rng.uniform(0, 1)), float(rng.uniform(0, 1)),
+              float(rng.uniform(0.2, 1)), float(rng.uniform(0, 1))]
+        params, sd = F.pack_params(*pv), int(rng.integers(0, 1 << 62))
+        cfg = dict(world=world, h=h, w=w, steps=steps, window=window, attach=attach, peer=peer)
+        try:
+            ref = F.FireBatch((h, w), 1, max_steps=steps, with_jacobian=attach)
+            ref.set_params(params)
+            ref.set_seeds([sd])
+            ref.reset(init)
+            ref.run(F.DeviceLandscape.from_environment(env), steps, attach=[attach] * steps,
+                    window=window)
+            rb, rd = ref.unpack()
+            shards = []
+            for r in range(world):
+                sh = RowShard(RowPartition(h, world, r), env.elevation, env.wind_speed,
+                              env.wind_direction, env.canopy, env.density, init, max_steps=steps,
+                              with_jacobian=attach)
+                sh.batch.set_params(params)
+                sh.batch.set_seeds([sd])
+                shards.append(sh)
+            if peer:
+                connect_local_peers(shards)
+                run_peer_local(shards, steps, window=window, attach=[attach] * steps)
+            else:
+                run_sharded_local(shards, steps, window=window, attach=[attach] * steps)
+            torch.cuda.synchronize()
+            gb = torch.cat([sh.owned(sh.batch.unpack()[0][0]) for sh in shards])
+            gd = torch.cat([sh.owned(sh.batch.unpack()[1][0]) for sh in shards])
+            ok = (torch.equal(gb, rb[0]) and torch.equal(gd, rd[0]) and
+                  torch.equal(torch.cat([sh.owned(sh.batch.acc[0]) for sh in shards]), ref.acc[0]) and
+                  torch.equal(torch.cat([sh.owned(sh.batch.t_ign[0]) for sh in shards]), ref.t_ign[0]))
+        except Exception as exc:
+            ok = repr(exc)
+        if ok is not True:
+            failed.append((case, cfg, ok))
+            log("FAIL shards", case, cfg, ok)
+    return failed
+
+
 def main():
     cases = int(sys.argv[1]) if len(sys.argv) > 1 else 100
-    failed = fuzz(cases, int(sys.argv[2]) if len(sys.argv) > 2 else 0)
+    seed = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+    failed = fuzz(cases, seed)
     print(f"{cases - len(failed)}/{cases} configurations pass")
-    return 1 if failed else 0
+    nsh = max(1, cases // 10)
+    failed_sh = fuzz_shards(nsh, seed)
+    print(f"{nsh - len(failed_sh)}/{nsh} row-shard configurations pass")
+    return 1 if failed or failed_sh else 0
 
 
 if __name__ == "__main__":
