@@ -1132,3 +1132,38 @@ def test_integration_stub_runs_the_device_path():
         runs.append((b.planes.clone(), b.acc.clone(), grad))
     assert torch.equal(runs[0][0], runs[1][0]) and torch.equal(runs[0][1], runs[1][1])
     assert torch.equal(runs[0][2], runs[1][2])
+
+
+@pytest.mark.parametrize("rng", ["splitmix", "philox"])
+def test_dense_burning_regime(rng):
+    """Dense regime: half the cells burning at step 0 and p_continue 0.95,
+    so most work words are full and every tile is listed.  Windows
+    1/4/8/16, list and dense sweeps, attached or not, must give the same
+    bytes, and SplitMix member 0 must equal the oracle."""
+    h, w, steps = 140, 203, 24
+    env = S.make_environment(h, w, seed=21)
+    dl = F.DeviceLandscape.from_environment(env)
+    init = np.random.default_rng(4).random((h, w)) < 0.5
+    pv = (0.05, 0.12, 0.09, 0.3, 0.95)
+    runs = []
+    for window, skip, attach in [(1, True, False), (4, True, True), (8, True, False),
+                                 (16, True, True), (8, False, True)]:
+        b = F.FireBatch((h, w), 2, max_steps=steps, with_jacobian=attach)
+        b.set_params(F.pack_params(*pv))
+        b.set_seeds([9, 10])
+        b.reset(init)
+        b.run(dl, steps, attach=[attach] * steps, window=window, skip_inactive=skip, rng=rng)
+        bu, bd = b.unpack()
+        runs.append((bu, bd, b.acc.clone(), b.t_ign.clone(), b.series()))
+    base = runs[0]
+    assert int(base[0][0].sum()) > h * w // 5  # the regime: a large share still burning
+    for other in runs[1:]:
+        for x, y in zip(base[:4], other[:4]):
+            assert torch.equal(x, y)
+        assert np.array_equal(base[4], other[4])
+    if rng == "splitmix":
+        arr = S.reference_landscape_arrays(env, O.slope_from_altitude)
+        ref = O.run(**arr, params=P(pv), init=init, steps=steps, seed=9, attach_steps=())
+        assert np.array_equal(base[0][0].bool().cpu().numpy(), ref.burning)
+        assert np.array_equal(base[1][0].bool().cpu().numpy(), ref.burned)
+        np.testing.assert_allclose(base[2][0].double().cpu().numpy(), ref.acc, rtol=RTOL_ACC)
