@@ -19,7 +19,7 @@ def main():
     env = S.make_environment(H, seed=1)
     ph = S.ensemble_ph(M)
     params = [(0.045, 0.131, 0.078, float(p), 0.3) for p in ph]
-    runner = EnsembleRunner((H, W), M, STEPS)
+    runner = EnsembleRunner((H, W), M, STEPS, depth=int(os.environ.get("E2E_DEPTH", 2)))
     env_host = torch.stack([torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)) for a in
                             (env.elevation, env.wind_speed, env.wind_direction, env.canopy,
                              env.density)]).pin_memory()
@@ -27,17 +27,28 @@ def main():
     for _ in range(3):
         runner(env_host, init_host, params, list(range(M)))
     torch.cuda.synchronize()
+    # timing probes only (wrong results): E2E_PROBE=nolandscape / noexport
+    probe = os.environ.get("E2E_PROBE", "")
+    if probe == "nolandscape":
+        for sl in runner.slots:
+            sl.build_landscape = lambda *a: None
+    if probe == "noexport":
+        for sl in runner.slots:
+            sl.export = lambda *a: None
     n = 20
     t0 = time.perf_counter()
-    prev = None
+    # depth - 1 calls ahead of the host: call i's results are read after
+    # call i + depth - 1 is submitted
+    pending = []
     for _ in range(n):
-        tk = runner.submit(env_host, init_host, params, list(range(M)))
-        if prev is not None:
-            prev.result()
-        prev = tk
-    prev.result()
+        pending.append(runner.submit(env_host, init_host, params, list(range(M))))
+        if len(pending) >= len(runner.slots):
+            pending.pop(0).result()
+    for tk in pending:
+        tk.result()
     dt = (time.perf_counter() - t0) / n
-    print(f"{os.environ.get('FC_DF_CTAS', 'default')}: e2e {1e3 * dt:.3f} ms per call, "
+    knobs = {k: v for k, v in os.environ.items() if k.startswith(("FC_", "E2E_"))}
+    print(f"{knobs or 'default'}: e2e {1e3 * dt:.3f} ms per call, "
           f"{M * H * W * STEPS / dt:.3g} cell-updates/s")
 
 
