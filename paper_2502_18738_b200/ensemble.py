@@ -260,6 +260,15 @@ class EnsembleRunner:
         return self.submit(env_host, init_host, params, seeds, norm_c).result()
 
 
+def _graph_safe_collectives() -> bool:
+    """Whether the gradient all-reduce can live inside a CUDA graph: one
+    process, or an NCCL process group (gloo collectives run on the host)."""
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return True
+    return dist.get_backend() == "nccl"
+
+
 class EnsembleCalibrator:
     """Ensemble fwd+bwd calibration (BASELINE config 4) on this rank's
     members: every iteration re-simulates all members from the initial state
@@ -272,7 +281,7 @@ class EnsembleCalibrator:
                  obs_steps: Sequence[int], members: Sequence[int], params, *,
                  steps: Optional[int] = None, wind_schedule: Optional[torch.Tensor] = None,
                  lr: float = 1e-2, weight_decay: float = 0.0, window: Optional[int] = None,
-                 device=None):
+                 device=None, graph: bool = True):
         from .parallel import allreduce_sum_  # noqa: F401  (import check)
         self.land, self.lr, self.wd, self.window = land, lr, weight_decay, window
         self.steps = int(steps if steps is not None else max(obs_steps))
@@ -294,9 +303,31 @@ class EnsembleCalibrator:
         self.adam_step = torch.zeros((1,), dtype=torch.int32, device=dev)
         self.attach = [True] * self.steps
         self.last_loss = None
+        # iterations after the first replay one CUDA graph of the whole
+        # iteration (reset, the run, loss/gradient, all-reduce, AdamW): the
+        # host's per-launch work leaves the GPU's critical path
+        self.use_graph, self._graph = bool(graph) and _graph_safe_collectives(), None
 
     def step(self):
-        """One iteration; returns the (members, 2 + 2S) loss rows (device)."""
+        """One iteration; returns the (members, 2 + 2S) loss rows (device;
+        with graph=True the same tensor every iteration, rewritten in place)."""
+        if not self.use_graph:
+            return self._iteration()
+        if self._graph is None:
+            from .device import CapturedSequence
+            loss = self._iteration()
+            try:
+                # the capture records without executing (no second update)
+                self._graph = CapturedSequence(self._iteration, warmup=0)
+            except Exception:  # e.g. a collective that cannot be captured: stay eager
+                torch.cuda.synchronize(self.batch.device)
+                self.use_graph, self._graph = False, None
+            self.last_loss = loss if self._graph is None else self.last_loss
+            return loss
+        self._graph.replay()
+        return self.last_loss
+
+    def _iteration(self):
         from . import _lib as L
         from .parallel import allreduce_sum_
         b = self.batch

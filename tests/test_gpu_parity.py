@@ -1167,3 +1167,31 @@ def test_dense_burning_regime(rng):
         assert np.array_equal(base[0][0].bool().cpu().numpy(), ref.burning)
         assert np.array_equal(base[1][0].bool().cpu().numpy(), ref.burned)
         np.testing.assert_allclose(base[2][0].double().cpu().numpy(), ref.acc, rtol=RTOL_ACC)
+
+
+def test_ensemble_calibrator_graph_replay_equals_eager():
+    """EnsembleCalibrator replays one CUDA graph per iteration after the
+    first: four graph iterations give the same losses and shared parameters,
+    bit for bit, as four eager ones (reset parity, lazy reset, AdamW step
+    count all live on the device or repeat per iteration)."""
+    from paper_2502_18738_b200.device import wind_ramp_schedule
+    from paper_2502_18738_b200.ensemble import EnsembleCalibrator
+    h, w, steps = 96, 80, 24
+    env = S.make_environment(h, w, seed=9)
+    dl = F.DeviceLandscape.from_environment(env)
+    sched = wind_ramp_schedule(steps, 2.0, 12.0, 90.0)
+    init = S.center_ignition(h, w)
+    targets = np.zeros((2, h, w), bool)
+    targets[0, 40:56, 32:50] = True
+    targets[1, 30:66, 24:58] = True
+    runs = []
+    for graph in (False, True):
+        cal = EnsembleCalibrator(dl, init, torch.as_tensor(targets), [12, 24], [0, 1, 2, 3],
+                                 (0.045, 0.131, 0.078, 0.58, 0.3), steps=steps,
+                                 wind_schedule=sched, lr=5e-2, graph=graph)
+        losses = [cal.step().clone() for _ in range(4)]
+        assert cal._graph is None if not graph else cal._graph is not None
+        runs.append((torch.stack(losses), cal.shared.clone()))
+    assert torch.equal(runs[0][0], runs[1][0])
+    assert torch.equal(runs[0][1], runs[1][1])
+    assert not torch.equal(runs[0][0][0], runs[0][0][-1])  # the parameters moved

@@ -10,12 +10,16 @@ import bench  # noqa: E402
 from paper_2502_18738_b200 import ensemble  # noqa: E402
 
 w = os.environ.get("WINDOW")
-if w:
+gr = os.environ.get("C4_GRAPH")
+if w or gr:
     orig = ensemble.EnsembleCalibrator.__init__
 
     def init(self, *a, **k):
-        k["window"] = int(w)
+        if w:
+            k["window"] = int(w)
+        if gr:
+            k["graph"] = bool(int(gr))
         orig(self, *a, **k)
     ensemble.EnsembleCalibrator.__init__ = init
 r = bench.bench_ensemble_calibration(torch.device("cuda", 0), 0, 1, iters=5)
-print(os.environ.get("FC_DATAFLOW"), "window", w, "c4 it/s %.1f ms %.3f" % (r["iter_per_s"], r["ms_per_iter"]))
+print(os.environ.get("FC_DATAFLOW"), "window", w, "graph", gr, "c4 it/s %.1f ms %.3f" % (r["iter_per_s"], r["ms_per_iter"]))
