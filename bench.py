@@ -885,6 +885,39 @@ def bench_dense(dev, peak):
                                              "bytes": sbytes, "achieved_GBps": ach_s,
                                              "frac_of_peak": ach_s / peak, "live_tiles": live}
         del b
+    # every cell active: a random half of the domain burning at step 0, burning
+    # on (p_continue 0.999: each burning cell still draws every step), ignition
+    # of the rest within a few steps -- every tile is live in every launch and
+    # every cell takes a continue draw per step.  Dense sweep (the mode that
+    # takes dense tiles' draws in the sweep), K = 8, one warm-up launch
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(11)
+    half = (torch.rand((n, n), generator=gen, device=dev) < 0.5).to(torch.uint8)
+    nl = 4
+    b = F.FireBatch((n, n), 1, max_steps=WINDOW * (nl + 1), device=dev)
+    b.set_params(F.pack_params(0.045, 0.131, 0.078, 0.2, 0.999))
+    b.set_seeds([3])
+    b.reset(half)
+    b.run(dl, WINDOW, window=WINDOW, skip_inactive=False)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    b.run(dl, WINDOW * nl, window=WINDOW, skip_inactive=False)
+    e1.record()
+    torch.cuda.synchronize()
+    ms_l = e0.elapsed_time(e1) / nl
+    burning = int(b.series()[0, -1, 0])
+    cups = n * n * WINDOW / (ms_l / 1e3)
+    cap = peak * 1e9 / 18.0
+    out["regime_all_active"] = {
+        "ms_per_launch": ms_l, "cell_updates_per_s": cups, "launches": nl,
+        "burning_cells_at_end": burning, "cells": n * n,
+        "survey_dense_cap_cu_per_s": cap, "frac_of_survey_dense_cap": cups / cap,
+        "bound": "issue (SplitMix64 continue draws, 56 instructions per draw; ncu: 68 % of "
+                 "issue slots busy, 0.1 % of DRAM; profiles/r2_ncu_summary.md section 14)",
+        "setup": "16384^2, a random half burning at step 0, p_continue 0.999, p_h 0.2, dense "
+                 "sweep, K = 8: every tile live, every cell drawn every step"}
+    del b, half
     out["note"] = ("dense = every launch rescans the whole domain (fc_activity_scan, one fused "
                    "kernel: the burning plane read once, quiet tiles' next state written as zeros "
                    "= 256 B per 32x32 "

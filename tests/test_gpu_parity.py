@@ -1146,8 +1146,11 @@ def test_dense_burning_regime(rng):
     init = np.random.default_rng(4).random((h, w)) < 0.5
     pv = (0.05, 0.12, 0.09, 0.3, 0.95)
     runs = []
+    # dense sweeps (skip False) with 4- and 8-step windows take dense tiles'
+    # continue draws in the sweep (FC_DENSE_TILE_MIN)
     for window, skip, attach in [(1, True, False), (4, True, True), (8, True, False),
-                                 (16, True, True), (8, False, True)]:
+                                 (16, True, True), (8, False, True), (4, False, False),
+                                 (16, False, False)]:
         b = F.FireBatch((h, w), 2, max_steps=steps, with_jacobian=attach)
         b.set_params(F.pack_params(*pv))
         b.set_seeds([9, 10])
