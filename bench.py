@@ -591,7 +591,7 @@ def bench_calibration(dev):
             "effective_frac_survey": 1826.0 * n * n * iters / (ms / 1e3) / 1e9 / load_peaks()[0]}
 
 
-def bench_ensemble_calibration(dev, rank, world, members_total=256, iters=3):
+def bench_ensemble_calibration(dev, rank, world, members_total=256, iters=10):
     """Config 4: 256 members x 1024^2 x 200 steps, all steps attached, wind
     rotating +90 deg and ramping 2 -> 12 m/s (device schedule), per-member
     4-target loss + gradient, gradients summed over members and all-reduced
