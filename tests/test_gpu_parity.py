@@ -1165,6 +1165,21 @@ def test_dense_burning_regime(rng):
             assert torch.equal(x, y)
         assert np.array_equal(base[4], other[4])
     if rng == "splitmix":
+        # draw injection of the same draws (the reference's uniform_grid
+        # tensors) through the dense sweep's in-sweep draws: same bytes
+        draws = np.stack([np.stack([np.stack([O.uniform_grid(sd, t, ch, 0, 0, h, w)
+                                              for ch in (0, 1)]) for sd in (9, 10)])
+                          for t in range(steps)])
+        for window in (4, 8):
+            b = F.FireBatch((h, w), 2, max_steps=steps)
+            b.set_params(F.pack_params(*pv))
+            b.set_seeds([9, 10])
+            b.reset(init)
+            b.run(dl, steps, window=window, skip_inactive=False, rng="inject",
+                  draws=torch.as_tensor(draws, device=b.device))
+            bu, bd = b.unpack()
+            assert torch.equal(bu, base[0]) and torch.equal(bd, base[1])
+            assert torch.equal(b.acc, base[2]) and torch.equal(b.t_ign, base[3])
         arr = S.reference_landscape_arrays(env, O.slope_from_altitude)
         ref = O.run(**arr, params=P(pv), init=init, steps=steps, seed=9, attach_steps=())
         assert np.array_equal(base[0][0].bool().cpu().numpy(), ref.burning)
