@@ -209,6 +209,16 @@ int fc_state_reset(const fc_grid* g, const fc_state* s, const uint8_t* init,
 int fc_state_unpack(const fc_grid* g, const fc_state* s, int32_t phase, uint8_t* burning,
                     uint8_t* burned, fc_stream_t stream);
 
+/* Jaccard index per member of the affected cells (burning | burned) against a
+ * uint8 target mask [H][W] per member (member_stride elements apart; 0 = one
+ * mask shared by all members): out[m] = |A & T| / |A | T|, 1 when both are
+ * empty -- the metric of calibration.py's iteration records, computed from the
+ * bit planes (no unpack).  work: 2 M + 1 zero-initialised uint64 on the device,
+ * left zeroed by the call.  Replaces jaccard_index (pyrocell/losses.py:89-98)
+ * over unpacked grids in calibrate()'s records (calibration.py:204). */
+int fc_state_jaccard(const fc_grid* g, const fc_state* s, int32_t phase, const uint8_t* targets,
+                     int64_t member_stride, uint64_t* work, double* out, fc_stream_t stream);
+
 /* Export the current state into [M][H][W] result arrays: burning / burned as
  * uint8 0/1 and the accumulator as fp32 (any may be NULL) -- the same values
  * fc_state_unpack and the acc plane hold.  The arrays may be pinned host

@@ -32,7 +32,7 @@ NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", 
 EXPORTS = ("fc_grid_make", "fc_plane_words", "fc_loss_workspace_bytes", "fc_sched_workspace_bytes",
            "fc_state_init",
            "fc_state_reset",
-           "fc_state_unpack", "fc_state_export", "fc_state_rebase", "fc_host_device_pointer", "fc_inject", "fc_run", "fc_run_pass", "fc_mark_ghosts", "fc_peer_signal", "fc_stream_wait_geq", "fc_activity_scan",
+           "fc_state_unpack", "fc_state_jaccard", "fc_state_export", "fc_state_rebase", "fc_host_device_pointer", "fc_inject", "fc_run", "fc_run_pass", "fc_mark_ghosts", "fc_peer_signal", "fc_stream_wait_geq", "fc_activity_scan",
            "fc_contract", "fc_recompute64", "fc_contract_steps", "fc_loss_grad",
            "fc_loss_dense", "fc_adamw", "fc_uniform_grid", "fc_epoch_seed", "fc_build_fields",
            "fc_landscape_build", "fc_landscape_build_ctas",
@@ -113,6 +113,7 @@ def lib():
             "fc_state_init": (C.c_int, [G, ST, vp, i64, i32, vp]),
             "fc_state_reset": (C.c_int, [G, ST, vp, i64, i32, vp]),
             "fc_state_unpack": (C.c_int, [G, ST, i32, vp, vp, vp]),
+            "fc_state_jaccard": (C.c_int, [G, ST, i32, vp, i64, vp, vp, vp]),
             "fc_state_export": (C.c_int, [G, ST, i32, vp, vp, vp, vp, vp]),
             "fc_host_device_pointer": (C.c_int, [vp, C.POINTER(vp)]),
             "fc_inject": (C.c_int, [G, ST, vp, i32, i32, i32, vp]),

@@ -498,6 +498,26 @@ class FireBatch:
                                         L.ptr(d), L.stream_ptr(stream)), "fc_state_unpack")
         return b, d
 
+    def jaccard(self, targets: torch.Tensor, out: Optional[torch.Tensor] = None, stream=None):
+        """fc_state_jaccard: per-member Jaccard index (losses.py:89-98) of the
+        affected cells (burning | burned) against uint8/bool targets (H, W)
+        shared by all members, or (M, H, W); from the bit planes, on the
+        device.  Returns a float64 (M,) device tensor (out, if given)."""
+        t = targets if targets.dtype == torch.uint8 else targets.to(torch.uint8)
+        t = t.to(self.device).contiguous()
+        if t.shape[-2:] != (self.h, self.w) or (t.dim() == 3 and t.shape[0] not in (1, self.m)):
+            raise ValueError(f"targets shape {tuple(t.shape)} does not match {(self.m, self.h, self.w)}")
+        stride = self.h * self.w if t.dim() == 3 and t.shape[0] == self.m and self.m > 1 else 0
+        if out is None:
+            out = torch.empty((self.m,), dtype=torch.float64, device=self.device)
+        if getattr(self, "_jaccard_work", None) is None:
+            self._jaccard_work = torch.zeros((2 * self.m + 1,), dtype=torch.int64, device=self.device)
+        st = self.struct()
+        L.check(L.lib().fc_state_jaccard(C.byref(self.grid), C.byref(st), self.q, L.ptr(t), stride,
+                                         L.ptr(self._jaccard_work), L.ptr(out),
+                                         L.stream_ptr(stream)), "fc_state_jaccard")
+        return out
+
     def export(self, burning, burned, acc, written=None, stream=None):
         """fc_state_export: the current state into (M, H, W) uint8 / uint8 /
         fp32 tensors (any may be None), on the device or pinned on the host

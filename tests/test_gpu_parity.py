@@ -1213,3 +1213,36 @@ def test_ensemble_calibrator_graph_replay_equals_eager():
     assert torch.equal(runs[0][0], runs[1][0])
     assert torch.equal(runs[0][1], runs[1][1])
     assert not torch.equal(runs[0][0][0], runs[0][0][-1])  # the parameters moved
+
+
+def test_state_jaccard_matches_reference_formula():
+    """fc_state_jaccard (bit planes, per member, shared or per-member targets)
+    equals losses.py:89-98's jaccard_index over the unpacked grids, including
+    the empty/empty case (1.0) and ragged tile edges; the work buffer is left
+    zeroed so consecutive calls agree."""
+    h, w, steps, M = 77, 133, 30, 3
+    env = S.make_environment(h, w, seed=13)
+    dl = F.DeviceLandscape.from_environment(env)
+    b = F.FireBatch((h, w), M, max_steps=steps)
+    b.set_params(F.pack_params(0.05, 0.12, 0.09, 0.62, 0.45))
+    b.set_seeds([1, 2, 3])
+    b.reset(S.center_ignition(h, w))
+    b.run(dl, steps)
+    bu, bd = b.unpack()
+    aff = (bu | bd).bool().cpu().numpy()
+    rng = np.random.default_rng(5)
+    shared = rng.random((h, w)) < 0.1
+    shared[30:50, 50:90] = True
+    per = rng.random((M, h, w)) < 0.05
+
+    def ref(a, t):
+        u = int(np.count_nonzero(a | t))
+        return 1.0 if u == 0 else int(np.count_nonzero(a & t)) / u
+    for _ in range(2):
+        got = b.jaccard(torch.as_tensor(shared)).cpu().numpy()
+        assert [float(x) for x in got] == [ref(aff[m], shared) for m in range(M)]
+    got = b.jaccard(torch.as_tensor(per)).cpu().numpy()
+    assert [float(x) for x in got] == [ref(aff[m], per[m]) for m in range(M)]
+    e = F.FireBatch((h, w), 1, max_steps=1)
+    e.reset(np.zeros((h, w), bool))
+    assert float(e.jaccard(torch.zeros((h, w), dtype=torch.uint8))[0]) == 1.0
