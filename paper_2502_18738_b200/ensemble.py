@@ -261,12 +261,12 @@ class EnsembleRunner:
 
 
 def _graph_safe_collectives() -> bool:
-    """Whether the gradient all-reduce can live inside a CUDA graph: one
-    process, or an NCCL process group (gloo collectives run on the host)."""
+    """Whether the iteration is captured as a CUDA graph: one process only.
+    With several ranks the all-reduce stays eager -- a capture that failed on
+    one rank and not on another would leave the ranks' collectives
+    mismatched (the graph saves ~1 % of a c4 iteration)."""
     import torch.distributed as dist
-    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
-        return True
-    return dist.get_backend() == "nccl"
+    return not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1
 
 
 class EnsembleCalibrator:
