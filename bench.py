@@ -486,16 +486,25 @@ def run_ours(args):
            "final_burning_member0": e2e_check}
 
     extras = {}
+
+    def extra(name, fn, *a):
+        # an extra that fails (on every rank alike: the same code and data)
+        # is reported in the line instead of taking the headline with it
+        try:
+            return fn(*a)
+        except Exception as exc:  # noqa: BLE001
+            torch.cuda.synchronize()
+            return {"error": f"{name}: {type(exc).__name__}: {exc}"[:300]}
     if not args.no_extras:
-        c4 = bench_ensemble_calibration(dev, rank, world)
-        c3 = bench_row_sharded(dev, rank, world)
+        c4 = extra("ensemble_calibration", bench_ensemble_calibration, dev, rank, world)
+        c3 = extra("row_sharded", bench_row_sharded, dev, rank, world)
         if rank == 0:
             extras["ensemble_calibration"] = c4
             extras["row_sharded"] = c3
     if rank == 0 and world == 1 and not args.no_extras:
-        extras["calibration"] = bench_calibration(dev)
-        extras["fig6_sweep"] = bench_fig6_sweep(dev)
-        extras["dense_probe"] = bench_dense(dev, peak)
+        extras["calibration"] = extra("calibration", bench_calibration, dev)
+        extras["fig6_sweep"] = extra("fig6_sweep", bench_fig6_sweep, dev)
+        extras["dense_probe"] = extra("dense_probe", bench_dense, dev, peak)
     cpu = None
     if rank == 0 and world == 1:
         cores = os.cpu_count() or 1
