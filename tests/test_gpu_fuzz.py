@@ -24,3 +24,13 @@ def test_random_row_shards_match_unsharded():
     from fuzz_parity import fuzz_shards
     failed = fuzz_shards(12, 7, log=lambda *a: None)
     assert not failed, failed[:5]
+
+
+def test_random_dense_configurations_match_plain_run_and_oracle():
+    """The sweep with half the cases started from a random 20-80 % burning
+    mask: the dense-tile paths (in-sweep continue draws of dense sweeps,
+    paired slot loops over crowded candidates) against the plain run and
+    the oracle."""
+    from fuzz_parity import fuzz
+    failed = fuzz(40, 11, log=lambda *a: None, dense=0.5)
+    assert not failed, failed[:3]

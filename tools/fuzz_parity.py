@@ -58,9 +58,13 @@ def check_loss(rng, b, res, h, w, steps):
     return ok_l and ok_g
 
 
-def fuzz(cases: int, seed: int, log=print):
-    """Run `cases` random configurations; returns the failing ones."""
+def fuzz(cases: int, seed: int, log=print, dense: float = 0.0):
+    """Run `cases` random configurations; returns the failing ones.  dense:
+    share of cases whose initial fire is a random mask of 20-80 % of the
+    cells (the dense-tile paths: in-sweep continue draws of dense sweeps),
+    drawn from a second generator so the default stream is unchanged."""
     rng = np.random.default_rng(seed)
+    rng_dense = np.random.default_rng(seed + 1000003)
     failed = []
     for case in range(cases):
         h, w = int(rng.integers(1, 261)), int(rng.integers(1, 261))
@@ -79,6 +83,8 @@ def fuzz(cases: int, seed: int, log=print):
             r, c = int(rng.integers(0, h)), int(rng.integers(0, w))
             k = int(rng.integers(1, 6))
             init[r:r + k, c:c + k] = True
+        if dense > 0 and rng_dense.random() < dense:
+            init = rng_dense.random((h, w)) < rng_dense.uniform(0.2, 0.8)
         seeds = [int(rng.integers(0, 1 << 62)) for _ in range(M)]
         params = F.pack_params(*pv)
         draw_rng = "philox" if rng.integers(0, 4) == 0 else "splitmix"
@@ -191,7 +197,8 @@ def fuzz_shards(cases: int, seed: int, log=print):
 def main():
     cases = int(sys.argv[1]) if len(sys.argv) > 1 else 100
     seed = int(sys.argv[2]) if len(sys.argv) > 2 else 0
-    failed = fuzz(cases, seed)
+    dense = float(os.environ.get("FUZZ_DENSE", "0"))
+    failed = fuzz(cases, seed, dense=dense)
     print(f"{cases - len(failed)}/{cases} configurations pass")
     nsh = max(1, cases // 10)
     failed_sh = fuzz_shards(nsh, seed)
