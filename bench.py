@@ -437,7 +437,12 @@ def run_ours(args):
                         "kernel is latency-bound (barrier and memory-latency stalls), "
                         "profiles/r2_ncu_summary.md"}
     # -------------------------------------------------------------- e2e
-    runner = EnsembleRunner((H, W), MEMBERS, STEPS, device=dev)
+    # three slots, results read two calls behind: call i+1's upload then
+    # overlaps call i-1's export instead of waiting for it on the host (two
+    # slots: 0.45-0.6 ms between every other pair of runs, 3.20 against
+    # 3.03-3.07 ms per call; profiles/r2_ncu_summary.md section 30)
+    E2E_DEPTH = 3
+    runner = EnsembleRunner((H, W), MEMBERS, STEPS, device=dev, depth=E2E_DEPTH)
     env_host = torch.stack([torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)) for a in
                             (env.elevation, env.wind_speed, env.wind_direction, env.canopy,
                              env.density)]).pin_memory()
@@ -445,13 +450,14 @@ def run_ours(args):
     for _ in range(max(len(runner.slots), args.warmup)):
         runner(env_host, init_host, params, members)
     barrier()
-    # K calls pipelined two deep (EnsembleRunner.submit): call i's results
-    # are read on the host while call i+1 uploads and runs; every call's
-    # H2D and D2H lies inside the timed region, L2 flushed between calls
+    # K calls pipelined three deep (EnsembleRunner.submit): call i-2's
+    # results are read on the host while call i-1 exports, call i runs and
+    # call i+1 uploads; every call's H2D and D2H lies inside the timed
+    # region, L2 flushed between calls
     flush()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    prev = None
+    pending = []
     # at least 40 calls: the host side of a call varies by up to ~0.2 ms
     # between runs, which 20 calls (66 ms) do not average out
     n_e2e = max(args.steps, 40)
@@ -462,13 +468,13 @@ def run_ours(args):
         # have produced)
         with torch.cuda.stream(runner.compute_stream):
             flush()
-        tk = runner.submit(env_host, init_host, params, members)
-        if prev is not None:
-            res = prev.result()
+        pending.append(runner.submit(env_host, init_host, params, members))
+        if len(pending) >= E2E_DEPTH:
+            res = pending.pop(0).result()
             e2e_check = int(res.series[0, -1, 0])  # read the result on the host
-        prev = tk
-    res = prev.result()
-    e2e_check = int(res.series[0, -1, 0])
+    for prev in pending:
+        res = prev.result()
+        e2e_check = int(res.series[0, -1, 0])
     e2e_total = allreduce_max(1e3 * (time.perf_counter() - t0), dev)
     cu_e2e = world * MEMBERS * CELL_UPDATES_PER_MEMBER * n_e2e
     e2e = {"value": cu_e2e / (e2e_total / 1e3), "unit": "cell-updates/s", "calls": n_e2e,
@@ -481,8 +487,8 @@ def run_ours(args):
                                                        runner.batch.grid.tiles_x * runner.batch.grid.tiles_y * MEMBERS,
                                                        runner.d2h_bytes_dense),
            "api": "paper_2502_18738_b200.ensemble.EnsembleRunner.submit (pinned host in/out, "
-                  "2-deep pipeline: upload of call i+1, kernels of call i and export of "
-                  "call i-1 on three streams)",
+                  "3-deep pipeline: upload of call i+1, kernels of call i and export of "
+                  "call i-1 on three streams, results of call i-2 read on the host)",
            "final_burning_member0": e2e_check}
 
     extras = {}
