@@ -50,6 +50,27 @@ def main():
         dur = ends - starts
         print(f"member {mm}: windows {len(ws)}, end {ends.max():.0f} us, window dur mean "
               f"{dur.mean():.1f} max {dur.max():.1f}, gap mean {gaps.mean():.2f} max {gaps.max():.2f} us")
+    ends_m = [en[m == mm].max() for mm in range(M)]
+    print("member end (us):", " ".join(f"{x:.0f}" for x in ends_m))
+    crit = int(np.argmax(ends_m))
+    sel = m == crit
+    ws = np.unique(w[sel])
+    rows = []
+    for x in ws:
+        s2 = sel & (w == x)
+        rows.append((x, s2.sum(), st[s2].min(), st[s2].max(), en[s2].min(), en[s2].max(),
+                     np.median(en[s2] - st[s2])))
+    print(f"critical member {crit}: window, groups, dispatch skew, dur, median group, gap to next")
+    for i, (x, ng, s0, s1, e0_, e1_, med) in enumerate(rows):
+        gap = rows[i + 1][2] - e1_ if i + 1 < len(rows) else 0.0
+        if i % 4 == 0 or i == len(rows) - 1:
+            print(f"  w{x:3d} ng {ng:3d} skew {s1 - s0:5.1f} dur {e1_ - s0:5.1f} "
+                  f"med {med:5.1f} gap {gap:5.2f}")
+    tot_gap = sum(rows[i + 1][2] - rows[i][5] for i in range(len(rows) - 1))
+    tot_skew = sum(r[3] - r[2] for r in rows)
+    tot_dur = sum(r[5] - r[2] for r in rows)
+    print(f"critical member totals: windows {tot_dur:.0f} us, of which dispatch skew {tot_skew:.0f}; "
+          f"gaps {tot_gap:.0f} us")
     # concurrency over time
     grid = np.linspace(0, en.max(), 20)
     conc = [int(np.sum((st <= x) & (en > x))) for x in grid]
