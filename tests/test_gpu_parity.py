@@ -674,9 +674,11 @@ def test_state_export_pinned_and_written_flags():
         g.export(torch.zeros((m, n, n), dtype=torch.uint8), None, None)  # not pinned
 
 
-def test_ensemble_runner_pipelined_submits():
-    """submit() tickets (depth-2 slot ring, copies overlapping the next
-    call) return the same results as synchronous calls, per submission."""
+@pytest.mark.parametrize("depth", [2, 3])
+def test_ensemble_runner_pipelined_submits(depth):
+    """submit() tickets (slot ring of 2 or 3, results read depth - 1 calls
+    behind as bench.py does, copies overlapping the next calls) return the
+    same results as synchronous calls, per submission."""
     from paper_2502_18738_b200.ensemble import EnsembleRunner
     n, m, steps = 128, 2, 40
     envs = []
@@ -692,15 +694,17 @@ def test_ensemble_runner_pipelined_submits():
     for k in range(5):
         o = ref(envs[k % 3], init, params, [k, k + 7])
         want.append([a.copy() for a in (o.burning, o.burned, o.accumulator, o.series)])
-    r = EnsembleRunner((n, n), m, steps, depth=2)
+    r = EnsembleRunner((n, n), m, steps, depth=depth)
     tickets, got = [], []
     for k in range(5):
         tickets.append(r.submit(envs[k % 3], init, params, [k, k + 7]))
-        if k >= 1:
-            o = tickets[k - 1].result()
+        if k >= depth - 1:
+            o = tickets[k - depth + 1].result()
             got.append([a.copy() for a in (o.burning, o.burned, o.accumulator, o.series)])
-    o = tickets[-1].result()
-    got.append([a.copy() for a in (o.burning, o.burned, o.accumulator, o.series)])
+    for tk in tickets[len(tickets) - depth + 1:]:
+        o = tk.result()
+        got.append([a.copy() for a in (o.burning, o.burned, o.accumulator, o.series)])
+    assert len(got) == 5
     for g, w in zip(got, want):
         for x, y in zip(g, w):
             np.testing.assert_array_equal(x, y)
